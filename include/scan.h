@@ -1,0 +1,149 @@
+/*
+ * scan.h -- C ABI of the B200 (sm_100a) device-wide prefix-sum library
+ * (libscan.so, built from paper_2505_15112_b200/csrc/).
+ *
+ * What the calls compute (PAPER.md = arxiv 2505.15112 "Parallel Scan on
+ * Ascend AI Accelerators"; "P<line>" cites its line):
+ *   - scan_inclusive: P68 (Sec. 2) "The inclusive prefix sum of a sequence
+ *     x_1, x_2, x_3, ... is the sequence x_1, x_1+x_2, x_1+x_2+x_3, ...".
+ *   - scan_exclusive: P461 (App. B.2) the inclusive output "shifted by one
+ *     element, discarding the last value and writing zero to the first
+ *     position".
+ *   - scan_rows: P437 (App. B.1) "The batched scan computes the prefix sum of
+ *     a batch of input arrays of equal length".
+ *   - scan_total / scan_carry_from_totals: the reduce step of Reduce-Scan-Scan
+ *     (P73, Sec. 2.1) applied at device level, so each GPU of a sharded
+ *     array can start its scan from the sum of all lower shards (DESIGN.md
+ *     "Multi-GPU").
+ *   - Type pairs: int32->int32, fp32->fp32, fp16->fp32 ("float16 (with
+ *     float32 output)", P98) and int8->int32 ("input matrices of 8-bit
+ *     integers with output/accumulation in 32-bit integers", P459).
+ *
+ * Arithmetic:
+ *   - Integer outputs wrap mod 2^32 (two's complement).  int8 input is summed
+ *     as signed values; 0/1 flags are the special case the paper uses.
+ *   - Float outputs: elements are summed in fp32 inside a tile and the
+ *     cross-tile carry is kept in fp64; each output is rounded to fp32 once
+ *     (round to nearest even).  Accuracy contract (BASELINE.json north_star):
+ *     |out_i - exact_i| <= 1e-6 * sum_{j<=i}|x_j| + 1e-6.
+ *
+ * Conventions for every call:
+ *   - Pointers named in/out/carry/total/ws are DEVICE pointers on the current
+ *     CUDA device.  The caller owns and frees every buffer; the library never
+ *     allocates device memory and keeps no pointer after it returns.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  All calls
+ *     only enqueue work on it and never synchronize the host.
+ *   - n == 0 (or rows == 0 / cols == 0) is a no-op returning SCAN_OK.
+ *   - Aliasing: in == out is allowed when input and output elements have the
+ *     same size (int32, fp32); any other overlap returns SCAN_ERR_ARG.
+ *   - Any element alignment is accepted; 16-byte-aligned arrays (and row
+ *     strides that are multiples of 16 bytes) take the TMA fast path.
+ *   - Errors: SCAN_ERR_ARG for a bad argument (n < 0, NULL pointer with
+ *     n > 0, unknown dtype, bad rank/G), SCAN_ERR_WORKSPACE for a workspace
+ *     that is NULL, too small or not 256-byte aligned (an uninitialised
+ *     workspace cannot be detected: see scan_workspace_init),
+ *     SCAN_ERR_DEVICE if the current device is not sm_100, SCAN_ERR_CUDA if
+ *     a CUDA call or launch failed.  Nothing is enqueued when an error is
+ *     returned before the launch.  No call aborts or throws.
+ *   - Workspace: one caller-owned device buffer of scan_workspace_bytes()
+ *     bytes, initialised ONCE with scan_workspace_init() before first use,
+ *     then reusable by any number of calls issued in stream order.  Two
+ *     calls that may run concurrently must not share a workspace.
+ *   - Thread safety: calls are reentrant; the library's only state is a
+ *     per-device cache of device attributes.
+ */
+#ifndef PAPER_2505_15112_B200_SCAN_H
+#define PAPER_2505_15112_B200_SCAN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCAN_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define SCAN_API __attribute__((visibility("default")))
+#else
+#define SCAN_API
+#endif
+
+/* Input -> output element types. */
+typedef enum {
+    SCAN_I32_I32 = 0,   /* int32 in, int32 out                 */
+    SCAN_F32_F32 = 1,   /* fp32 in, fp32 out                   */
+    SCAN_F16_F32 = 2,   /* IEEE binary16 in, fp32 out (P98)    */
+    SCAN_I8_I32 = 3     /* int8 in (signed), int32 out (P459)  */
+} scan_dtype;
+
+typedef enum {
+    SCAN_OK = 0,
+    SCAN_ERR_ARG = 1,
+    SCAN_ERR_WORKSPACE = 2,
+    SCAN_ERR_CUDA = 3,
+    SCAN_ERR_DEVICE = 4
+} scan_status;
+
+/* SCAN_ABI_VERSION of the loaded library. */
+SCAN_API int scan_abi_version(void);
+
+/* Static string for a status code (never NULL). */
+SCAN_API const char* scan_status_string(int status);
+
+/* Bytes of workspace a 1-D scan of n elements of `dtype` needs (also enough
+ * for scan_total of n elements).  Returns 0 for an invalid dtype or n < 0. */
+SCAN_API size_t scan_workspace_bytes(int dtype, int64_t n);
+
+/* Bytes of workspace scan_rows(rows, cols) needs. */
+SCAN_API size_t scan_rows_workspace_bytes(int dtype, int64_t rows, int64_t cols);
+
+/* Initialise a workspace of ws_bytes bytes (enqueued on `stream`).  Must be
+ * called once after allocation and before the first scan that uses it. */
+SCAN_API int scan_workspace_init(void* ws, size_t ws_bytes, void* stream);
+
+/* Inclusive scan (P68): out[i] = c + in[0] + ... + in[i], n elements.
+ * carry_in: NULL (c = 0) or a device pointer to ONE value added in front of
+ * the sequence: int64_t for integer dtypes (used mod 2^32), double for
+ * float dtypes.  It is how a shard of a larger array continues the scan of
+ * the shards before it. */
+SCAN_API int scan_inclusive(const void* in, void* out, int64_t n, int dtype, const void* carry_in,
+                   void* ws, size_t ws_bytes, void* stream);
+
+/* Exclusive scan (P461): out[0] = c, out[i] = c + in[0] + ... + in[i-1].
+ * Same arguments as scan_inclusive. */
+SCAN_API int scan_exclusive(const void* in, void* out, int64_t n, int dtype, const void* carry_in,
+                   void* ws, size_t ws_bytes, void* stream);
+
+/* Row-batched scan (P437): for r in [0, rows), the `cols` elements at
+ * in + r*in_row_stride are scanned independently (inclusive, or exclusive if
+ * `exclusive` != 0) into out + r*out_row_stride.  Strides are in ELEMENTS of
+ * the input / output type and must be >= cols. */
+SCAN_API int scan_rows(const void* in, void* out, int64_t rows, int64_t cols, int64_t in_row_stride,
+              int64_t out_row_stride, int dtype, int exclusive, void* ws, size_t ws_bytes,
+              void* stream);
+
+/* Reduction of n input elements (the "R" of Reduce-Scan-Scan, P73):
+ * *total_out = in[0] + ... + in[n-1] as int64_t (integer dtypes, exact) or
+ * double (float dtypes, fp64 accumulation in a fixed order, so repeated calls
+ * give identical bits).  total_out is a device pointer. */
+SCAN_API int scan_total(const void* in, int64_t n, int dtype, void* total_out, void* ws,
+               size_t ws_bytes, void* stream);
+
+/* Carry of shard `rank` of G contiguous shards: *carry_out = totals[0] + ...
+ * + totals[rank-1], summed in that order (0 for rank 0).  totals holds G
+ * device values of the scan_total type (int64_t or double); carry_out gets
+ * one value of the same type, ready for scan_inclusive's carry_in. */
+SCAN_API int scan_carry_from_totals(const void* totals, int G, int rank, int dtype, void* carry_out,
+                           void* stream);
+
+/* Kernel launches the library enqueued since load (a process-wide counter;
+ * used by the bench to report how many of its own kernels ran). */
+SCAN_API uint64_t scan_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PAPER_2505_15112_B200_SCAN_H */

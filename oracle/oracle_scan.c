@@ -35,6 +35,10 @@
  *      result is ONE round-to-nearest-even conversion of that double.  The
  *      tolerance weight A_i = sum_{j<=i} |x_j| (BASELINE.json north_star) is
  *      accumulated beside it, also in double.
+ *   R6 with a carry-in c (which stands for the sum of the elements before
+ *      this array, e.g. lower shards) the weight starts at |c|:
+ *      A_i = |c| + sum_{j<=i} |x_j|, a lower bound of the weight the same
+ *      element has in the unsharded array.
  *   R5 fp16 is decoded from its IEEE-754 binary16 bit layout here (sign,
  *      5-bit exponent, 10-bit fraction, subnormals, inf/NaN) so the oracle
  *      does not depend on any CUDA conversion routine.
@@ -102,7 +106,8 @@ typedef struct {
 void oracle_fstate_init(oracle_fstate* st, double carry_in, int has_carry)
 {
     st->sum = has_carry ? carry_in : 0.0;
-    st->abs_sum = 0.0;
+    st->abs_sum = has_carry ? fabs(carry_in) : 0.0;   /* R6: the carry stands for the
+                                                         elements before this array */
     st->count = 0;
     st->has_carry = has_carry;
 }

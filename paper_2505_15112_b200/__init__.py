@@ -1,0 +1,216 @@
+"""B200-native device-wide prefix sum (scan): thin Python binding of libscan.so.
+
+The product is the C ABI in ``include/scan.h`` (built from ``csrc/`` for
+sm_100a).  This module only marshals torch tensors (device memory) and the
+current CUDA stream into those calls; every step of the scan runs in the CUDA
+kernels.  There is no CPU fallback: if ``libscan.so`` is missing or the device
+is not a B200, the calls raise.
+
+Public API (names follow the C ABI):
+    inclusive(x, out=None, carry_in=None)     -- P68 inclusive prefix sum
+    exclusive(x, out=None, carry_in=None)     -- P461 exclusive prefix sum
+    rows(X, exclusive=False, out=None)        -- P437 batched row scan
+    total(x)                                  -- RSS reduction (P73)
+    carry_from_totals(totals, rank)           -- sum of lower shard totals
+    sharded_inclusive / sharded_exclusive     -- see paper_2505_15112_b200.dist
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libscan.so")
+
+SCAN_I32_I32, SCAN_F32_F32, SCAN_F16_F32, SCAN_I8_I32 = 0, 1, 2, 3
+_STATUS = {0: "SCAN_OK", 1: "SCAN_ERR_ARG", 2: "SCAN_ERR_WORKSPACE", 3: "SCAN_ERR_CUDA",
+           4: "SCAN_ERR_DEVICE"}
+
+# input torch dtype -> (scan dtype code, output torch dtype, total/carry dtype)
+DTYPES = {
+    torch.int32: (SCAN_I32_I32, torch.int32, torch.int64),
+    torch.float32: (SCAN_F32_F32, torch.float32, torch.float64),
+    torch.float16: (SCAN_F16_F32, torch.float32, torch.float64),
+    torch.int8: (SCAN_I8_I32, torch.int32, torch.int64),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+class ScanError(RuntimeError):
+    pass
+
+
+def load() -> ctypes.CDLL:
+    """Load the in-tree libscan.so (build it with ``make -C paper_2505_15112_b200``)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ScanError(f"{LIB_PATH} not built; run __graft_entry__.build() or "
+                            f"make -C {_HERE}")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I64, I, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t
+        L.scan_abi_version.restype = I
+        L.scan_status_string.argtypes = [I]
+        L.scan_status_string.restype = ctypes.c_char_p
+        L.scan_workspace_bytes.argtypes = [I, I64]
+        L.scan_workspace_bytes.restype = SZ
+        L.scan_rows_workspace_bytes.argtypes = [I, I64, I64]
+        L.scan_rows_workspace_bytes.restype = SZ
+        L.scan_workspace_init.argtypes = [P, SZ, P]
+        L.scan_workspace_init.restype = I
+        for f in (L.scan_inclusive, L.scan_exclusive):
+            f.argtypes = [P, P, I64, I, P, P, SZ, P]
+            f.restype = I
+        L.scan_rows.argtypes = [P, P, I64, I64, I64, I64, I, I, P, SZ, P]
+        L.scan_rows.restype = I
+        L.scan_total.argtypes = [P, I64, I, P, P, SZ, P]
+        L.scan_total.restype = I
+        L.scan_carry_from_totals.argtypes = [P, I, I, I, P, P]
+        L.scan_carry_from_totals.restype = I
+        L.scan_launch_count.restype = ctypes.c_uint64
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = load().scan_status_string(rc).decode()
+        raise ScanError(f"{what}: {msg}")
+
+
+def _stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+class Workspace:
+    """A caller-owned, initialised workspace (device uint8 buffer).
+
+    One per (device, stream) is cached by ``workspace()``; it grows on demand
+    and is re-initialised (scan_workspace_init) whenever it is reallocated."""
+
+    def __init__(self, nbytes: int, device, stream=None):
+        nbytes = max(int(nbytes), 1 << 16)
+        self.buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+        off = (-self.buf.data_ptr()) % 256
+        self.nbytes = nbytes
+        self.ptr = self.buf.data_ptr() + off
+        _check(load().scan_workspace_init(ctypes.c_void_p(self.ptr), nbytes, _stream_ptr(stream)),
+               "scan_workspace_init")
+
+
+_ws_cache: dict = {}
+
+
+def workspace(nbytes: int, device=None, stream=None) -> Workspace:
+    dev = torch.device(device) if device is not None else torch.device("cuda",
+                                                                       torch.cuda.current_device())
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    key = (dev.index, s.cuda_stream)
+    ws = _ws_cache.get(key)
+    if ws is None or ws.nbytes < nbytes:
+        ws = Workspace(max(nbytes, 2 * (ws.nbytes if ws else 0)), dev, s)
+        _ws_cache[key] = ws
+    return ws
+
+
+def _prep(x: torch.Tensor):
+    if not x.is_cuda:
+        raise ScanError("input must be a CUDA tensor (there is no CPU path)")
+    if x.dtype not in DTYPES:
+        raise ScanError(f"unsupported input dtype {x.dtype}; use int32, float32, float16, int8")
+    return DTYPES[x.dtype]
+
+
+def _scan1d(x: torch.Tensor, out, carry_in, exclusive: bool, stream=None):
+    dt, odt, cdt = _prep(x)
+    if x.dim() != 1:
+        raise ScanError("1-D scan expects a 1-D tensor; use rows() for batches")
+    if not x.is_contiguous():
+        raise ScanError("input must be contiguous")
+    n = x.numel()
+    if out is None:
+        out = torch.empty(n, dtype=odt, device=x.device)
+    elif out.dtype != odt or out.numel() != n or not out.is_contiguous():
+        raise ScanError(f"out must be a contiguous {odt} tensor of {n} elements")
+    if carry_in is not None and (carry_in.dtype != cdt or not carry_in.is_cuda):
+        raise ScanError(f"carry_in must be a CUDA {cdt} tensor")
+    L = load()
+    ws = workspace(L.scan_workspace_bytes(dt, n), x.device, stream)
+    fn = L.scan_exclusive if exclusive else L.scan_inclusive
+    _check(fn(_ptr(x), _ptr(out), n, dt, _ptr(carry_in), ctypes.c_void_p(ws.ptr), ws.nbytes,
+              _stream_ptr(stream)), "scan_exclusive" if exclusive else "scan_inclusive")
+    return out
+
+
+def inclusive(x: torch.Tensor, out=None, carry_in=None, stream=None) -> torch.Tensor:
+    """Inclusive prefix sum (P68) of a 1-D CUDA tensor; int32 or fp32 result."""
+    return _scan1d(x, out, carry_in, False, stream)
+
+
+def exclusive(x: torch.Tensor, out=None, carry_in=None, stream=None) -> torch.Tensor:
+    """Exclusive prefix sum (P461): out[0] = carry (0), out[i] = sum of x[:i]."""
+    return _scan1d(x, out, carry_in, True, stream)
+
+
+def rows(X: torch.Tensor, exclusive: bool = False, out=None, stream=None) -> torch.Tensor:
+    """Scan every row of a 2-D CUDA tensor independently (P437).  Rows may be
+    strided (row stride >= cols, unit column stride)."""
+    dt, odt, _ = _prep(X)
+    if X.dim() != 2 or (X.shape[1] > 1 and X.stride(1) != 1):
+        raise ScanError("rows() expects a 2-D tensor with unit column stride")
+    R, C = X.shape
+    if out is None:
+        out = torch.empty((R, C), dtype=odt, device=X.device)
+    elif out.dtype != odt or tuple(out.shape) != (R, C) or (C > 1 and out.stride(1) != 1):
+        raise ScanError(f"out must be a {odt} tensor of shape {(R, C)} with unit column stride")
+    in_stride = X.stride(0) if R > 1 else C
+    out_stride = out.stride(0) if R > 1 else C
+    L = load()
+    ws = workspace(L.scan_rows_workspace_bytes(dt, R, C), X.device, stream)
+    _check(L.scan_rows(_ptr(X), _ptr(out), R, C, max(in_stride, C), max(out_stride, C), dt,
+                       int(bool(exclusive)), ctypes.c_void_p(ws.ptr), ws.nbytes,
+                       _stream_ptr(stream)), "scan_rows")
+    return out
+
+
+def total(x: torch.Tensor, out=None, stream=None) -> torch.Tensor:
+    """Sum of a 1-D CUDA tensor: int64 (integer inputs) or fp64 (float inputs)."""
+    dt, _, cdt = _prep(x)
+    if out is None:
+        out = torch.empty(1, dtype=cdt, device=x.device)
+    L = load()
+    ws = workspace(L.scan_workspace_bytes(dt, 0), x.device, stream)
+    _check(L.scan_total(_ptr(x), x.numel(), dt, _ptr(out), ctypes.c_void_p(ws.ptr), ws.nbytes,
+                        _stream_ptr(stream)), "scan_total")
+    return out
+
+
+def carry_from_totals(totals: torch.Tensor, rank: int, in_dtype: torch.dtype, out=None,
+                      stream=None) -> torch.Tensor:
+    """totals[0] + ... + totals[rank-1] (device), ready to use as carry_in."""
+    dt, _, cdt = DTYPES[in_dtype]
+    if totals.dtype != cdt:
+        raise ScanError(f"totals must be {cdt}")
+    if out is None:
+        out = torch.empty(1, dtype=cdt, device=totals.device)
+    _check(load().scan_carry_from_totals(_ptr(totals), totals.numel(), rank, dt, _ptr(out),
+                                         _stream_ptr(stream)), "scan_carry_from_totals")
+    return out
+
+
+def launch_count() -> int:
+    return int(load().scan_launch_count())

@@ -1,0 +1,622 @@
+// scan_kernels.cuh -- sm_100a kernels of the device-wide prefix sum.
+//
+// What is computed (PAPER.md, "P<line>"): the inclusive prefix sum of P68
+// (Sec. 2), the exclusive one of P461 (App. B.2), the batched row scan of
+// P437 (App. B.1), with the P98/P459 type pairs.
+//
+// How: the paper's multi-core MCScan (Alg. 3, P229-261)
+// reads the input twice and writes it twice across a SyncAll barrier (3N+2N
+// traffic).  On B200 we use the single-pass "decoupled look-back" strategy
+// that the paper itself names as the GPU state of the art (P78-81, Sec. 2.1:
+// "require only ~2N data movement"):
+//
+//   a1  persistent CTAs claim tiles in order with a global atomic ticket;
+//   a2  a producer thread streams each tile HBM -> shared memory with a TMA
+//       1-D bulk copy (cp.async.bulk + mbarrier), STAGES tiles ahead;
+//   a3  the tile is scanned in registers: 4 elements per lane per 128-element
+//       row, a warp shuffle scan per row, rows chained within the warp, and
+//       a block scan of the warp totals (the analog of the cube's A@U_s
+//       row-local scans plus the vector unit's `partial` propagation of
+//       Alg. 1, P145-155);
+//   a4  warp 0 publishes the tile aggregate, looks back over the predecessor
+//       descriptors (32 per step, one per lane) until it meets an inclusive
+//       prefix, and publishes its own inclusive prefix (this replaces
+//       SyncAll + "Sum first i entries of r", P245-248);
+//   a5  outputs = carry + local prefix are written to a shared staging buffer
+//       and streamed back with a TMA bulk store.
+//
+// Integer tiles use uint32 arithmetic (wraps mod 2^32).  Float tiles use fp32
+// in-tile sums and an fp64 carry; an output is fl32(P_hi + fl32(base + l))
+// where (P_hi, P_lo) is the double-float split of the fp64 prefix folded
+// into the per-row base (an fp32 carry chain fails C2).
+//
+// Descriptor protocol (no fences needed): every 8-byte descriptor slot holds
+// (epoch << 32 | 32 payload bits) and is written once per call, so a reader
+// that sees its own epoch in a slot has a complete value.  fp64 values use
+// two slots (hi/lo words).  The epoch lives in the workspace header and is
+// advanced by the last CTA to finish, which also resets the ticket counter,
+// so no memset is needed between calls.
+#pragma once
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "ptx.cuh"
+
+namespace scan {
+
+// ---------------------------------------------------------------- workspace
+constexpr uint32_t kWsMagic = 0x5CA7B200u;
+constexpr size_t kWsPartialsOffset = 256;         // scan_total per-CTA partials
+constexpr int kMaxTotalCtas = 2048;
+constexpr size_t kWsDescOffset = kWsPartialsOffset + 8 * kMaxTotalCtas;  // 16640
+
+struct WsHeader {
+    uint32_t magic;
+    uint32_t epoch;         // tag of the current call's descriptors (>= 1)
+    uint32_t ticket;        // next tile to claim
+    uint32_t done;          // CTAs finished in the current call
+    uint32_t capacity;      // descriptor slots (tiles) the workspace holds
+    uint32_t total_done;    // scan_total: CTAs finished
+    uint32_t error;         // set if a kernel found a bad header
+    uint32_t pad[57];
+};
+static_assert(sizeof(WsHeader) == 256, "header is 256 bytes");
+
+// ---------------------------------------------------------------- type traits
+template <int DT>
+struct Traits;
+
+template <>
+struct Traits<0> {  // SCAN_I32_I32
+    using In = int32_t;
+    using Out = int32_t;
+    using Acc = uint32_t;
+    using Carry = uint32_t;
+    static constexpr bool kFloat = false;
+};
+template <>
+struct Traits<1> {  // SCAN_F32_F32
+    using In = float;
+    using Out = float;
+    using Acc = float;
+    using Carry = double;
+    static constexpr bool kFloat = true;
+};
+template <>
+struct Traits<2> {  // SCAN_F16_F32 (raw binary16 bits in)
+    using In = uint16_t;
+    using Out = float;
+    using Acc = float;
+    using Carry = double;
+    static constexpr bool kFloat = true;
+};
+template <>
+struct Traits<3> {  // SCAN_I8_I32
+    using In = int8_t;
+    using Out = int32_t;
+    using Acc = uint32_t;
+    using Carry = uint32_t;
+    static constexpr bool kFloat = false;
+};
+
+// ---- widening loads of 4 consecutive input elements (exact conversions) ----
+__device__ __forceinline__ void unpack4(const int32_t* s, uint32_t (&v)[4])
+{
+    uint4 q = *reinterpret_cast<const uint4*>(s);
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+}
+__device__ __forceinline__ void unpack4(const float* s, float (&v)[4])
+{
+    float4 q = *reinterpret_cast<const float4*>(s);
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+}
+__device__ __forceinline__ void unpack4(const uint16_t* s, float (&v)[4])
+{
+    uint2 q = *reinterpret_cast<const uint2*>(s);
+    __half2 a = *reinterpret_cast<__half2*>(&q.x);
+    __half2 b = *reinterpret_cast<__half2*>(&q.y);
+    float2 fa = __half22float2(a), fb = __half22float2(b);
+    v[0] = fa.x; v[1] = fa.y; v[2] = fb.x; v[3] = fb.y;
+}
+__device__ __forceinline__ void unpack4(const int8_t* s, uint32_t (&v)[4])
+{
+    uint32_t w = *reinterpret_cast<const uint32_t*>(s);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = (uint32_t)(int32_t)(int8_t)(w >> (8 * k));
+}
+__device__ __forceinline__ uint32_t widen(int32_t x) { return (uint32_t)x; }
+__device__ __forceinline__ uint32_t widen(int8_t x) { return (uint32_t)(int32_t)x; }
+__device__ __forceinline__ float widen(float x) { return x; }
+__device__ __forceinline__ float widen(uint16_t x) { return __half2float(__ushort_as_half(x)); }
+
+__device__ __forceinline__ void store4(int32_t* d, const uint32_t (&o)[4])
+{
+    *reinterpret_cast<uint4*>(d) = make_uint4(o[0], o[1], o[2], o[3]);
+}
+__device__ __forceinline__ void store4(float* d, const float (&o)[4])
+{
+    *reinterpret_cast<float4*>(d) = make_float4(o[0], o[1], o[2], o[3]);
+}
+__device__ __forceinline__ int32_t narrow(uint32_t x, int32_t*) { return (int32_t)x; }
+__device__ __forceinline__ float narrow(float x, float*) { return x; }
+
+// ---- warp primitives -------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T x, int lane)
+{
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        T y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x = x + y;
+    }
+    return x;
+}
+
+__device__ __forceinline__ uint32_t warp_sum(uint32_t x) { return __reduce_add_sync(0xffffffffu, x); }
+__device__ __forceinline__ double warp_sum(double x)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// ---- look-back descriptors -------------------------------------------------
+// int: 2 slots per tile {aggregate, inclusive}; fp64: 4 slots {agg hi, agg lo,
+// incl hi, incl lo}.  Slot = (epoch << 32) | payload.
+template <typename Carry>
+struct Desc;
+
+template <>
+struct Desc<uint32_t> {
+    static constexpr int kSlots = 2;
+    static __device__ __forceinline__ void publish(uint64_t* d, bool inclusive, uint32_t tag,
+                                                   uint32_t v)
+    {
+        ptx::st_relaxed_u64(d + (inclusive ? 1 : 0), ((uint64_t)tag << 32) | v);
+    }
+    // status: 2 = inclusive prefix, 1 = aggregate, 0 = not ready.
+    static __device__ __forceinline__ int read(const uint64_t* d, uint32_t tag, uint32_t& v)
+    {
+        uint64_t a, i;
+        ptx::ld_relaxed_v2u64(d, a, i);
+        if ((uint32_t)(i >> 32) == tag) { v = (uint32_t)i; return 2; }
+        if ((uint32_t)(a >> 32) == tag) { v = (uint32_t)a; return 1; }
+        v = 0;
+        return 0;
+    }
+};
+
+template <>
+struct Desc<double> {
+    static constexpr int kSlots = 4;
+    static __device__ __forceinline__ void publish(uint64_t* d, bool inclusive, uint32_t tag,
+                                                   double v)
+    {
+        uint64_t b = (uint64_t)__double_as_longlong(v);
+        uint64_t t = (uint64_t)tag << 32;
+        ptx::st_relaxed_v2u64(d + (inclusive ? 2 : 0), t | (b >> 32), t | (b & 0xffffffffull));
+    }
+    static __device__ __forceinline__ int read(const uint64_t* d, uint32_t tag, double& v)
+    {
+        uint64_t ah, al, ih, il;
+        ptx::ld_relaxed_v2u64(d, ah, al);
+        ptx::ld_relaxed_v2u64(d + 2, ih, il);
+        if ((uint32_t)(ih >> 32) == tag && (uint32_t)(il >> 32) == tag) {
+            v = __longlong_as_double((long long)((ih << 32) | (il & 0xffffffffull)));
+            return 2;
+        }
+        if ((uint32_t)(ah >> 32) == tag && (uint32_t)(al >> 32) == tag) {
+            v = __longlong_as_double((long long)((ah << 32) | (al & 0xffffffffull)));
+            return 1;
+        }
+        v = 0.0;
+        return 0;
+    }
+};
+
+// Warp-cooperative decoupled look-back for tile t of a segment whose first
+// tile is seg_first.  Returns the exclusive prefix of the tile (carry_seg +
+// all aggregates of tiles seg_first..t-1).  All 32 lanes call it.
+template <typename Carry>
+__device__ __forceinline__ Carry lookback(const uint64_t* desc, int64_t t, int64_t seg_first,
+                                          Carry carry_seg, uint32_t tag, int lane)
+{
+    using D = Desc<Carry>;
+    Carry excl = Carry(0);
+    int64_t pred = t - 1;
+    uint32_t backoff = 32;
+    while (true) {
+        int64_t idx = pred - lane;
+        int st;
+        Carry v;
+        if (idx >= seg_first) {
+            st = D::read(desc + idx * D::kSlots, tag, v);
+        } else {
+            st = 2;  // the virtual tile before the segment holds the carry-in
+            v = (idx == seg_first - 1) ? carry_seg : Carry(0);
+        }
+        uint32_t pm = __ballot_sync(0xffffffffu, st == 2);
+        uint32_t xm = __ballot_sync(0xffffffffu, st == 0);
+        uint32_t need = pm ? ((pm & (0u - pm)) << 1) - 1u : 0xffffffffu;  // lanes 0..first P
+        if (xm & need) {
+            __nanosleep(backoff);
+            backoff = backoff < 1024 ? backoff * 2 : 1024;
+            continue;
+        }
+        Carry c = ((need >> lane) & 1u) ? v : Carry(0);
+        excl = excl + warp_sum(c);
+        if (pm) return excl;
+        pred -= 32;
+    }
+}
+
+// ---------------------------------------------------------------- parameters
+struct ScanParams {
+    const void* in;
+    void* out;
+    int64_t seg_len;        // elements per segment (n for 1-D, cols for rows)
+    int64_t num_segs;       // 1 for 1-D, rows for scan_rows
+    int64_t in_stride;      // elements between segment starts (input)
+    int64_t out_stride;     // elements between segment starts (output)
+    int64_t tiles_per_seg;
+    int64_t num_tiles;
+    const void* carry_in;   // nullable; applies to segment 0 (1-D API only)
+    uint8_t* ws;            // workspace (unused when static_sched)
+    int exclusive;
+    int tma_in;             // segment bases and strides 16-byte aligned (input)
+    int tma_out;            // same for output
+    int static_sched;       // one tile per segment: no tickets, no look-back
+};
+
+template <int THREADS, int ROWS>
+struct TileShape {
+    static constexpr int kWarps = THREADS / 32;
+    static constexpr int kRowElems = 128;                 // 32 lanes x 4 elements
+    static constexpr int kWarpElems = ROWS * kRowElems;
+    static constexpr int kTile = kWarps * kWarpElems;     // elements per tile
+};
+
+// Dynamic shared memory of k_scan_tiles.
+template <int DT, int THREADS, int ROWS, int STAGES, int OSTAGES>
+constexpr size_t scan_smem_bytes()
+{
+    using T = Traits<DT>;
+    return (size_t)STAGES * TileShape<THREADS, ROWS>::kTile * sizeof(typename T::In) +
+           (size_t)OSTAGES * TileShape<THREADS, ROWS>::kTile * sizeof(typename T::Out);
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int DT, int THREADS, int ROWS, int STAGES, int OSTAGES, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p)
+{
+    using Tr = Traits<DT>;
+    using In = typename Tr::In;
+    using Out = typename Tr::Out;
+    using Acc = typename Tr::Acc;
+    using Carry = typename Tr::Carry;
+    using Shape = TileShape<THREADS, ROWS>;
+    constexpr int NW = Shape::kWarps;
+    constexpr int TILE = Shape::kTile;
+
+    extern __shared__ __align__(128) uint8_t smem[];
+    In* const in_stage = reinterpret_cast<In*>(smem);
+    Out* const out_stage = reinterpret_cast<Out*>(smem + (size_t)STAGES * TILE * sizeof(In));
+
+    __shared__ __align__(8) uint64_t full_bar[STAGES];
+    __shared__ int64_t s_ticket[STAGES];
+    __shared__ int s_tma[STAGES];
+    __shared__ Acc s_warp_tot[NW];
+    __shared__ Acc s_warp_pref[NW];
+    __shared__ Carry s_prefix;
+    __shared__ uint32_t s_epoch;
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+
+    WsHeader* hdr = reinterpret_cast<WsHeader*>(p.ws);
+    uint64_t* desc = reinterpret_cast<uint64_t*>(p.ws + kWsDescOffset);
+    const In* gin = reinterpret_cast<const In*>(p.in);
+    Out* gout = reinterpret_cast<Out*>(p.out);
+
+    uint64_t pol_in = 0, pol_out = 0;
+    int64_t static_next = blockIdx.x;
+
+    // Claim the next tile and, if it can go by TMA, start streaming it into stage s.
+    auto issue = [&](int s) {
+        int64_t t;
+        if (p.static_sched) {
+            t = static_next;
+            static_next += gridDim.x;
+        } else {
+            t = (int64_t)atomicAdd(&hdr->ticket, 1u);
+        }
+        s_ticket[s] = t;
+        int tma = 0;
+        if (t < p.num_tiles) {
+            int64_t seg = t / p.tiles_per_seg;
+            int64_t k = t - seg * p.tiles_per_seg;
+            int64_t m = p.seg_len - k * TILE;
+            if (m > TILE) m = TILE;
+            uint32_t bytes = (uint32_t)(m * (int64_t)sizeof(In));
+            if (p.tma_in && (bytes & 15u) == 0) {
+                tma = 1;
+                ptx::mbar_arrive_expect_tx(&full_bar[s], bytes);
+                ptx::tma_load_1d(in_stage + (size_t)s * TILE, gin + seg * p.in_stride + k * TILE, bytes,
+                                 &full_bar[s], pol_in);
+            }
+        }
+        s_tma[s] = tma;
+    };
+
+    if (tid == 0) {
+        if (!p.static_sched) {
+            if (hdr->magic != kWsMagic) hdr->error = 1;
+            s_epoch = hdr->epoch;
+        }
+        pol_in = ptx::policy_evict_first();
+        pol_out = ptx::policy_evict_first();
+        for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&full_bar[s], 1);
+        ptx::fence_mbar_init();
+        for (int s = 0; s < STAGES; ++s) issue(s);
+    }
+    __syncthreads();
+    const uint32_t tag = s_epoch;
+
+    uint32_t phases = 0;  // bit s = parity of the next wait on full_bar[s]
+    int ostage = 0;
+    for (int64_t iter = 0;; ++iter) {
+        const int s = (int)(iter % STAGES);
+        const int64_t t = s_ticket[s];
+        if (t >= p.num_tiles) break;
+        const int tma = s_tma[s];
+        const int64_t seg = t / p.tiles_per_seg;
+        const int64_t k = t - seg * p.tiles_per_seg;
+        int64_t m64 = p.seg_len - k * TILE;
+        const int m = (int)(m64 > TILE ? TILE : m64);
+        const bool full = (m == TILE);
+        const In* src = gin + seg * p.in_stride + k * TILE;
+        Out* dst = gout + seg * p.out_stride + k * TILE;
+
+        // ---- a2: load the tile into registers (4 elements per lane per row)
+        Acc v[ROWS][4];
+        const int wbase = warp * Shape::kWarpElems + 4 * lane;
+        if (tma) {
+            ptx::mbar_wait(&full_bar[s], (phases >> s) & 1u);
+            phases ^= 1u << s;
+            const In* st = in_stage + (size_t)s * TILE;
+#pragma unroll
+            for (int j = 0; j < ROWS; ++j) unpack4(st + wbase + j * 128, v[j]);
+            if (!full) {
+#pragma unroll
+                for (int j = 0; j < ROWS; ++j)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (wbase + j * 128 + q >= m) v[j][q] = Acc(0);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < ROWS; ++j)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    int e = wbase + j * 128 + q;
+                    v[j][q] = e < m ? widen(src[e]) : Acc(0);
+                }
+        }
+
+        // ---- a3: thread-local, warp and row scans
+        Acc lane_excl[ROWS];
+        Acc row_tot[ROWS];
+#pragma unroll
+        for (int j = 0; j < ROWS; ++j) {
+            v[j][1] = v[j][0] + v[j][1];
+            v[j][2] = v[j][1] + v[j][2];
+            v[j][3] = v[j][2] + v[j][3];
+            Acc incl = warp_incl_scan(v[j][3], lane);
+            Acc ex = __shfl_up_sync(0xffffffffu, incl, 1);
+            lane_excl[j] = lane == 0 ? Acc(0) : ex;
+            row_tot[j] = __shfl_sync(0xffffffffu, incl, 31);
+        }
+        Acc row_pref[ROWS];
+        Acc wsum = Acc(0);
+#pragma unroll
+        for (int j = 0; j < ROWS; ++j) {
+            row_pref[j] = wsum;
+            wsum = wsum + row_tot[j];
+        }
+        if (lane == 0) s_warp_tot[warp] = wsum;
+        __syncthreads();  // [A] stage s fully read; warp totals visible
+
+        // Refill stage s with the next claimed tile while we finish this one.
+        if (tid == 0) issue(s);
+
+        // ---- a4: block scan of warp totals + decoupled look-back (warp 0)
+        if (warp == 0) {
+            Acc x = lane < NW ? s_warp_tot[lane] : Acc(0);
+            Acc xi = warp_incl_scan(x, lane);
+            Acc xe = __shfl_up_sync(0xffffffffu, xi, 1);
+            if (lane < NW) s_warp_pref[lane] = lane == 0 ? Acc(0) : xe;
+            const Acc agg = __shfl_sync(0xffffffffu, xi, NW - 1);
+            Carry carry_seg = Carry(0);
+            if (seg == 0 && p.carry_in != nullptr) {
+                if constexpr (Tr::kFloat)
+                    carry_seg = *reinterpret_cast<const double*>(p.carry_in);
+                else
+                    carry_seg = (uint32_t)(uint64_t)(*reinterpret_cast<const int64_t*>(p.carry_in));
+            }
+            Carry prefix;
+            if (k == 0) {
+                prefix = carry_seg;
+                if (!p.static_sched && p.tiles_per_seg > 1 && lane == 0)
+                    Desc<Carry>::publish(desc + t * Desc<Carry>::kSlots, true, tag,
+                                         carry_seg + Carry(agg));
+            } else {
+                if (lane == 0)
+                    Desc<Carry>::publish(desc + t * Desc<Carry>::kSlots, false, tag, Carry(agg));
+                prefix = lookback<Carry>(desc, t, t - k, carry_seg, tag, lane);
+                if (lane == 0 && k + 1 < p.tiles_per_seg)
+                    Desc<Carry>::publish(desc + t * Desc<Carry>::kSlots, true, tag,
+                                         prefix + Carry(agg));
+            }
+            if (lane == 0) s_prefix = prefix;
+        }
+        // The output staging buffer we are about to fill must no longer be
+        // read by the bulk store issued OSTAGES tiles ago.
+        if (tid == 0 && p.tma_out) ptx::bulk_wait_read<OSTAGES - 1>();
+        __syncthreads();  // [B] prefix and warp prefixes visible
+
+        // ---- a5: epilogue
+        const Carry P = s_prefix;
+        const Acc wpref = s_warp_pref[warp];
+        const bool use_tma_out = p.tma_out && ((m * (int)sizeof(Out)) & 15) == 0;
+        Out* ost = out_stage + (size_t)ostage * TILE;
+#pragma unroll
+        for (int j = 0; j < ROWS; ++j) {
+            Acc o[4];
+            if constexpr (Tr::kFloat) {
+                const float P_hi = (float)P;
+                const float P_lo = (float)(P - (double)P_hi);
+                const float base = P_lo + ((wpref + row_pref[j]) + lane_excl[j]);
+                if (p.exclusive) {
+                    o[0] = P_hi + base;
+                    o[1] = P_hi + (base + v[j][0]);
+                    o[2] = P_hi + (base + v[j][1]);
+                    o[3] = P_hi + (base + v[j][2]);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) o[q] = P_hi + (base + v[j][q]);
+                }
+            } else {
+                const Acc base = P + wpref + row_pref[j] + lane_excl[j];
+                if (p.exclusive) {
+                    o[0] = base;
+                    o[1] = base + v[j][0];
+                    o[2] = base + v[j][1];
+                    o[3] = base + v[j][2];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) o[q] = base + v[j][q];
+                }
+            }
+            const int e = wbase + j * 128;
+            if (use_tma_out) {
+                store4(ost + e, o);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (e + q < m) dst[e + q] = narrow(o[q], (Out*)nullptr);
+            }
+        }
+        if (use_tma_out) {
+            ptx::fence_proxy_async_smem();
+            __syncthreads();  // [C] staging buffer complete
+            if (tid == 0) {
+                ptx::tma_store_1d(dst, ost, (uint32_t)(m * (int)sizeof(Out)), pol_out);
+                ptx::bulk_commit();
+            }
+            ostage = (ostage + 1) % OSTAGES;
+        } else {
+            __syncthreads();  // keep the per-tile barrier count uniform
+        }
+    }
+
+    if (tid == 0) {
+        ptx::bulk_wait<0>();  // all stores done before the CTA (and its smem) retires
+        if (!p.static_sched) {
+            __threadfence();
+            uint32_t prev = atomicAdd(&hdr->done, 1u);
+            if (prev == gridDim.x - 1) {
+                // Last CTA: every other CTA has claimed its final ticket and
+                // read the epoch.  Reset the counters and advance the epoch.
+                hdr->ticket = 0;
+                hdr->done = 0;
+                uint32_t e = hdr->epoch + 1;
+                if (e == 0) {
+                    // Tag wrap (once per 2^32 calls): clear every slot so no
+                    // stale tag can match a recycled epoch.
+                    uint64_t nslots = (uint64_t)hdr->capacity * (Tr::kFloat ? 4 : 2);
+                    for (uint64_t i = 0; i < nslots; ++i) desc[i] = 0;
+                    e = 1;
+                }
+                hdr->epoch = e;
+                __threadfence();
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- reduction
+// scan_total: fixed partition of [0, n) into gridDim.x contiguous chunks;
+// per-thread sums in int64 / fp64, block reduction, then the last CTA adds
+// the per-CTA partials in index order (deterministic).
+template <int DT, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_total(const void* in_, int64_t n, void* total_out,
+                                                   uint8_t* ws)
+{
+    using Tr = Traits<DT>;
+    using In = typename Tr::In;
+    using Sum = typename std::conditional<Tr::kFloat, double, long long>::type;
+    const In* in = reinterpret_cast<const In*>(in_);
+    WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
+    Sum* partials = reinterpret_cast<Sum*>(ws + kWsPartialsOffset);
+
+    int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+    int64_t lo = (int64_t)blockIdx.x * chunk;
+    int64_t hi = lo + chunk < n ? lo + chunk : n;
+    Sum acc = 0;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += THREADS) {
+        if constexpr (Tr::kFloat)
+            acc += (double)widen(in[i]);
+        else
+            acc += (long long)(int32_t)widen(in[i]);
+    }
+    // block reduction (fixed order)
+    __shared__ Sum s_part[THREADS / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Sum b = 0;
+        for (int w = 0; w < THREADS / 32; ++w) b += s_part[w];
+        partials[blockIdx.x] = b;
+        __threadfence();
+        uint32_t prev = atomicAdd(&hdr->total_done, 1u);
+        if (prev == gridDim.x - 1) {
+            __threadfence();
+            Sum t = 0;
+            for (unsigned c = 0; c < gridDim.x; ++c) t += ((volatile Sum*)partials)[c];
+            *reinterpret_cast<Sum*>(total_out) = t;
+            hdr->total_done = 0;
+        }
+    }
+}
+
+// carry_r = totals[0] + ... + totals[rank-1], in that order.
+template <typename Sum>
+__global__ void k_carry_from_totals(const Sum* totals, int rank, Sum* carry_out)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        Sum c = 0;
+        for (int r = 0; r < rank; ++r) c += totals[r];
+        *carry_out = c;
+    }
+}
+
+__global__ void k_ws_init(uint8_t* ws, uint32_t capacity)
+{
+    WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        hdr->magic = kWsMagic;
+        hdr->epoch = 1;
+        hdr->ticket = 0;
+        hdr->done = 0;
+        hdr->capacity = capacity;
+        hdr->total_done = 0;
+        hdr->error = 0;
+    }
+}
+
+}  // namespace scan

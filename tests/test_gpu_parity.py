@@ -1,0 +1,223 @@
+"""Parity of the CUDA scan (through the C ABI) against the CPU oracle.
+
+Integers: bit-exact.  Floats: the north_star tolerance
+|gpu - oracle_fp64| <= 1e-6 * sum_{j<=i}|x_j| + 1e-6, element by element.
+Sizes span several tiles (8192 elements) and ragged tails; edge cases cover
+empty, 1 element, unaligned pointers, in-place, carry-in, strided rows.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+M32 = (1 << 32) - 1
+TORCH_IN = {"i32": torch.int32, "f32": torch.float32, "f16": torch.float16, "i8": torch.int8}
+NP_IN = {"i32": np.int32, "f32": np.float32, "f16": np.uint16, "i8": np.int8}
+
+
+def host_input(inputs_mod, dt, n, seed=123, kind=None):
+    if kind is None:
+        kind = {"i32": inputs_mod.I32_FULL, "f32": inputs_mod.F32_NORMAL,
+                "f16": inputs_mod.F16_NORMAL, "i8": inputs_mod.I8_FULL}[dt]
+    return inputs_mod.fill_host(kind, seed, 0, n)
+
+
+def to_dev(x, dt):
+    t = torch.from_numpy(np.ascontiguousarray(x))
+    if dt == "f16":
+        t = t.view(torch.float16)
+    return t.cuda()
+
+
+def oracle_1d(oracle, x, dt, exclusive, carry=None):
+    fn = oracle.exclusive if exclusive else oracle.inclusive
+    return fn(x, dt, carry_in=carry)
+
+
+def assert_parity(oracle, got, ref, dt):
+    got = got.cpu().numpy().reshape(-1)
+    if dt in ("i32", "i8"):
+        assert got.dtype == np.int32
+        bad = np.nonzero(got != ref.reshape(-1))[0]
+        assert bad.size == 0, f"{bad.size} mismatches, first at {bad[:5]}: {got[bad[:5]]} vs {ref.reshape(-1)[bad[:5]]}"
+    else:
+        y64, a64, _ = ref
+        bad, worst, at = oracle.check_f32(got, y64, a64)
+        assert bad == 0, f"{bad} elements out of tolerance; worst err/tol {worst} at {at}"
+        return worst
+
+
+SIZES = [1, 2, 3, 31, 32, 33, 127, 128, 129, 4095, 4096, 4097, 8191, 8192, 8193,
+         3 * 8192 + 5, 65536, 65537, 100003, 1 << 20, (1 << 20) + 3]
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_1d_sizes(cuda, oracle, inputs_mod, dt, exclusive):
+    for n in SIZES:
+        x = host_input(inputs_mod, dt, n, seed=n)
+        fn = cuda.exclusive if exclusive else cuda.inclusive
+        got = fn(to_dev(x, dt))
+        torch.cuda.synchronize()
+        assert_parity(oracle, got, oracle_1d(oracle, x, dt, exclusive), dt)
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+def test_random_sizes_and_carry(cuda, oracle, inputs_mod, dt):
+    rng = np.random.default_rng(7)
+    for trial in range(6):
+        n = int(rng.integers(1, 1 << 22))
+        x = host_input(inputs_mod, dt, n, seed=trial)
+        exclusive = bool(trial % 2)
+        if dt in ("i32", "i8"):
+            c = int(rng.integers(-(1 << 40), 1 << 40))
+            carry = torch.tensor([c], dtype=torch.int64, device="cuda")
+        else:
+            c = float(rng.normal() * 1000)
+            carry = torch.tensor([c], dtype=torch.float64, device="cuda")
+        fn = cuda.exclusive if exclusive else cuda.inclusive
+        got = fn(to_dev(x, dt), carry_in=carry)
+        torch.cuda.synchronize()
+        assert_parity(oracle, got, oracle_1d(oracle, x, dt, exclusive, carry=c), dt)
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+def test_unaligned(cuda, oracle, inputs_mod, dt):
+    n = 50000
+    for off_in in (0, 1, 2, 3):
+        for off_out in (0, 1, 3):
+            if off_in == 0 and off_out == 0:
+                continue
+            x = host_input(inputs_mod, dt, n + off_in, seed=off_in)
+            xd = to_dev(x, dt)[off_in:]
+            outb = torch.empty(n + off_out, dtype=torch.int32 if dt in ("i32", "i8")
+                               else torch.float32, device="cuda")
+            out = outb[off_out:]
+            cuda.inclusive(xd, out=out)
+            torch.cuda.synchronize()
+            assert_parity(oracle, out, oracle_1d(oracle, x[off_in:], dt, False), dt)
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32"])
+def test_in_place(cuda, oracle, inputs_mod, dt):
+    n = 300007
+    x = host_input(inputs_mod, dt, n)
+    xd = to_dev(x, dt)
+    cuda.inclusive(xd, out=xd)
+    torch.cuda.synchronize()
+    assert_parity(oracle, xd, oracle_1d(oracle, x, dt, False), dt)
+
+
+def test_empty_and_errors(cuda):
+    L = cuda.load()
+    x = torch.empty(0, dtype=torch.int32, device="cuda")
+    assert cuda.inclusive(x).numel() == 0
+    # bad arguments are rejected without launching
+    assert L.scan_inclusive(None, None, 10, 0, None, None, 0, None) == 1
+    assert L.scan_inclusive(None, None, -1, 0, None, None, 0, None) == 1
+    y = torch.zeros(100000, dtype=torch.int32, device="cuda")
+    z = torch.zeros(100000, dtype=torch.int32, device="cuda")
+    import ctypes
+    assert L.scan_inclusive(ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(z.data_ptr()),
+                            100000, 7, None, None, 0, None) == 1           # bad dtype
+    assert L.scan_inclusive(ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(z.data_ptr()),
+                            100000, 0, None, None, 0, None) == 2           # no workspace
+    assert L.scan_inclusive(ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(y.data_ptr() + 4),
+                            1000, 0, None, None, 0, None) == 1             # partial overlap
+
+
+def test_repeat_calls_reuse_workspace(cuda, oracle, inputs_mod):
+    """Epoch-tagged descriptors: 200 back-to-back calls on one workspace with
+    varying sizes must all be exact (no stale descriptor is ever read)."""
+    rng = np.random.default_rng(3)
+    xs = host_input(inputs_mod, "i32", 1 << 20, seed=99)
+    xd = to_dev(xs, "i32")
+    ref = oracle.inclusive(xs, "i32")
+    outs = []
+    for i in range(200):
+        n = int(rng.integers(8193, 1 << 20))
+        outs.append((n, cuda.inclusive(xd[:n])))
+    torch.cuda.synchronize()
+    for n, o in outs:
+        assert np.array_equal(o.cpu().numpy(), ref[:n])
+
+
+def test_float_bitwise_repeatable_c2_like(cuda, inputs_mod):
+    """fp16 U[0,1) (C2-like): fp64 carries are exact, so repeated runs give identical bits."""
+    n = 1 << 24
+    x = to_dev(inputs_mod.fill_host(inputs_mod.F16_U01, 1, 0, n), "f16")
+    a = cuda.inclusive(x)
+    b = cuda.inclusive(x)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+# ------------------------------------------------------------------ rows
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+def test_rows(cuda, oracle, inputs_mod, dt):
+    for R, C in ((1, 1), (7, 3), (5, 31), (148, 32), (7, 1000), (3, 4096), (5, 8192), (4, 8193),
+                 (9, 65536), (2, 131072), (300, 513)):
+        x = host_input(inputs_mod, dt, R * C, seed=R * 1000 + C).reshape(R, C)
+        for exc in (False, True):
+            got = cuda.rows(to_dev(x, dt), exclusive=exc)
+            torch.cuda.synchronize()
+            if dt in ("i32", "i8"):
+                ref = np.stack([oracle_1d(oracle, x[r], dt, exc) for r in range(R)])
+                assert_parity(oracle, got, ref, dt)
+            else:
+                parts = [oracle_1d(oracle, x[r], dt, exc) for r in range(R)]
+                ref = tuple(np.concatenate([p[k] for p in parts]) for k in range(3))
+                assert_parity(oracle, got, ref, dt)
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32"])
+def test_rows_strided(cuda, oracle, inputs_mod, dt):
+    R, C, S = 6, 20000, 20004
+    x = host_input(inputs_mod, dt, R * S).reshape(R, S)
+    xd = to_dev(x, dt)[:, :C]
+    outb = torch.empty((R, C + 8), dtype=torch.int32 if dt == "i32" else torch.float32,
+                       device="cuda")
+    out = outb[:, 3:3 + C]
+    cuda.rows(xd, out=out)
+    torch.cuda.synchronize()
+    for r in range(R):
+        assert_parity(oracle, out[r], oracle_1d(oracle, np.ascontiguousarray(x[r, :C]), dt, False),
+                      dt)
+
+
+def test_rows_exhaustive_12bit_flags(cuda, oracle):
+    """All 4096 length-12 0/1 flag patterns in one scan_rows call."""
+    pats = np.arange(4096)
+    X = ((pats[:, None] >> np.arange(12)[None, :]) & 1).astype(np.int8)
+    got = cuda.rows(to_dev(X, "i8")).cpu().numpy()
+    want = np.stack([oracle.inclusive(X[p], "i8") for p in range(4096)])
+    assert np.array_equal(got, want)
+    got = cuda.rows(to_dev(X, "i8"), exclusive=True).cpu().numpy()
+    want = np.stack([oracle.exclusive(X[p], "i8") for p in range(4096)])
+    assert np.array_equal(got, want)
+
+
+# ------------------------------------------------------------ total / carry
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+def test_total_and_carry(cuda, oracle, inputs_mod, dt):
+    for n in (1, 1000, 8193, 1 << 20, 12345677):
+        x = host_input(inputs_mod, dt, n, seed=n)
+        t = cuda.total(to_dev(x, dt))
+        torch.cuda.synchronize()
+        ref = oracle.total(x, dt)
+        if dt in ("i32", "i8"):
+            assert int(t.item()) == ref
+        else:
+            absum = oracle.FloatScan(dt)(x, want64=False, want32=False)[1][-1]
+            assert abs(t.item() - ref) <= 2 * n * 2.0 ** -53 * absum
+        t2 = cuda.total(to_dev(x, dt))
+        assert t2.item() == t.item()          # fixed summation order: identical bits
+    G = 5
+    cdt = torch.int64 if dt in ("i32", "i8") else torch.float64
+    totals = torch.tensor([3, -7, 11, 100, 5], dtype=cdt, device="cuda")
+    for r in range(G):
+        c = cuda.carry_from_totals(totals, r, TORCH_IN[dt])
+        assert c.item() == sum([3, -7, 11, 100, 5][:r])

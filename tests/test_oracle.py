@@ -173,8 +173,9 @@ def test_carry_in(oracle, inputs_mod):
     e = oracle.exclusive(x, "i32", carry_in=c)
     assert e[0] == c
     f = inputs_mod.fill_host(inputs_mod.F32_PM1, 4, 0, 10000)
-    y64, _, _ = oracle.inclusive(f, "f32", carry_in=1000.0)
-    assert np.array_equal(y64, 1000.0 + np.cumsum(f.astype(np.int64)))
+    y64, a64, _ = oracle.inclusive(f, "f32", carry_in=-1000.0)
+    assert np.array_equal(y64, -1000.0 + np.cumsum(f.astype(np.int64)))
+    assert np.array_equal(a64, 1000.0 + np.cumsum(np.abs(f.astype(np.int64))))   # R6
 
 
 def test_streaming_equals_whole(oracle, inputs_mod):
