@@ -1,0 +1,592 @@
+// mcscan.cuh -- the paper's multi-core scan (MCScan, Alg. 3, P229-261) with
+// its "L2 cache splitting" optimisation (Sec. 6.1.1, P332), re-designed for
+// B200 (sm_100a) as ONE persistent, cooperative kernel.
+//
+// Alg. 3 runs Phase I (per block: local scans + a recomputed block reduction
+// r_i, P235-243), a SyncAll barrier (P245), and Phase II (per block: partial =
+// sum of the first i entries of r, then propagate it through the block,
+// P247-254).  L2 splitting (P332) "splits the input into consecutive chunks so
+// that the input and intermediate arrays fit in the L2 cache during the
+// processing of each chunk ... the last value of each chunk is propagated to
+// the next chunk".  On B200 we keep the idea and change the mechanics:
+//
+//   * a chunk is G contiguous blocks of BT tiles, one block per CTA (G = SMs);
+//   * Phase I (job R(c)): each CTA streams its block HBM -> smem with TMA
+//     (L2 policy evict_last, so the bytes stay in the 126 MB L2) and reduces
+//     it to r[c][b];  it then arrives on the chunk's grid barrier;
+//   * Phase II (job S(c)): after the barrier, each CTA forms its carry
+//     (chunk carry + r[c][0..b-1] in a fixed order), re-reads its block -- now
+//     from L2 -- scans every tile in registers, adds the running carry and
+//     streams the result out with TMA bulk stores.  No local scans are ever
+//     written to global memory (Alg. 3 writes them to y in Phase I and reads
+//     them back in Phase II: 3N+2N traffic; here HBM sees N reads + N writes);
+//   * jobs run in the order R(0) R(1) S(0) R(2) S(1) ..., so the barrier of
+//     chunk c is normally complete long before S(c) needs it.
+//
+// Lanes: every compute lane owns 16 CONTIGUOUS elements, so one warp shuffle
+// scan serves 16 elements and the epilogue is one add per element.  Conflict-
+// free shared-memory access to 64 contiguous bytes per lane needs a swizzled
+// layout: 4-byte and 2-byte inputs (and all 4-byte outputs) move through TMA
+// *tensor* copies (cp.async.bulk.tensor.2d) over a [rows x 128 B] view of the
+// array with CU_TENSOR_MAP_SWIZZLE_128B, which stores 16-byte chunk c of tile
+// row R at chunk c ^ (R & 7).  int8 inputs (16 bytes per lane) use plain 1-D
+// bulk copies.  Elements past the last full 128-byte row are read / written
+// directly by the lanes that own them.
+//
+// Warp roles: warp 0 producer (TMA loads of the job sequence), warp 1 storer
+// (TMA stores), warp 2 coordinator (publishes r[c][b], waits for each chunk's
+// barrier and forms the block carries ahead of time), warps 3.. compute
+// (reductions and scans).  Carries: uint32 (ints, wraps mod 2^32) or fp64
+// (floats), as in k_scan_tiles.
+//
+// Grid barrier: one u32 arrival counter per chunk in a workspace region only
+// this kernel uses (zeroed by scan_workspace_init, reset by the last CTA).
+#pragma once
+#include <cuda.h>
+
+#include "scan_kernels.cuh"
+#include "scan_ws.cuh"  // mbar_wait_prof
+
+namespace scan {
+
+constexpr int kMcProf = 14;
+
+// Block reductions live in the workspace after the header: r[c][b] (8 bytes
+// each, chunk-major); barrier counters in their own region (kWsBarOffset).
+struct McGeom {
+    int64_t n;          // elements
+    int64_t tile;       // elements per tile
+    int64_t bt;         // tiles per block
+    int64_t block;      // elements per block = bt * tile
+    int64_t chunk;      // elements per chunk = G * block
+    int64_t chunks;     // number of chunks
+    int g;              // CTAs (blocks per chunk)
+};
+
+// Job q of a CTA's sequence R0 R1 S0 R2 S1 ... R(C-1) S(C-2) S(C-1):
+// returns the chunk and whether it is a scan (S) job.
+__device__ __forceinline__ void mc_job(int64_t q, int64_t chunks, int64_t& c, bool& is_scan)
+{
+    if (q == 0) { c = 0; is_scan = false; return; }
+    const int64_t k = q - 1;             // pairs (R(k/2+1), S(k/2)) ...
+    if (chunks == 1) { c = 0; is_scan = true; return; }
+    if (k < 2 * (chunks - 1)) {
+        c = (k & 1) ? (k >> 1) : (k >> 1) + 1;
+        is_scan = (k & 1) != 0;
+    } else {
+        c = chunks - 1;
+        is_scan = true;
+    }
+}
+
+
+
+struct McParams16 {
+    CUtensorMap tm_in;      // 2-D [rows x 128 B] view of the input (unused for int8)
+    CUtensorMap tm_out;     // 2-D [rows x 128 B] view of the output
+    const void* in;
+    void* out;
+    const void* carry_in;   // nullable: int64 (ints) / double (floats)
+    uint8_t* ws;
+    McGeom gm;
+    int64_t n_tma_in;       // elements covered by tm_in (full rows) / by bulk copies
+    int64_t n_tma_out;      // elements covered by tm_out (full rows)
+    int exclusive;
+    int debug;
+};
+
+template <int DT, int NC, int GPW, int NB_IN, int NB_OUT>
+struct Mc16Cfg {
+    using Tr = Traits<DT>;
+    using In = typename Tr::In;
+    static constexpr int kThreads = (3 + NC) * 32;
+    static constexpr int kTile = NC * GPW * 512;  // 32 lanes x 16 elements per group
+    static constexpr size_t kInSlot = (size_t)kTile * sizeof(In);
+    static constexpr size_t kOutSlot = (size_t)kTile * 4;
+    static constexpr int kRowElemsIn = 128 / (int)sizeof(In);          // elements per 128-B row
+    // TMA boxes: up to 256 rows of 128 B each (the box-dimension limit)
+    static constexpr int kBoxRowsIn = kInSlot / 128 < 256 ? (int)(kInSlot / 128) : 256;
+    static constexpr int kBoxRowsOut = kOutSlot / 128 < 256 ? (int)(kOutSlot / 128) : 256;
+    static constexpr int kBoxesIn = sizeof(In) == 1 ? 0 : (int)(kInSlot / (kBoxRowsIn * 128));
+    static constexpr int kBoxesOut = (int)(kOutSlot / (kBoxRowsOut * 128));
+    static_assert(sizeof(In) == 1 || kInSlot % (kBoxRowsIn * 128) == 0, "whole TMA boxes per tile");
+    static_assert(kOutSlot % (kBoxRowsOut * 128) == 0, "whole TMA boxes per tile");
+    static_assert(kBoxRowsIn % 8 == 0 && kBoxRowsOut % 8 == 0, "boxes keep the 1024-B swizzle phase");
+    static constexpr size_t kSmem = NB_IN * kInSlot + NB_OUT * kOutSlot + 1024;  // + alignment slack
+};
+
+// ---- 16 contiguous elements of lane-offset e0 from a swizzled slot -----------
+// 4-byte elements: row R = e0/32, half h = (e0/16)&1, chunks 4h..4h+3.
+__device__ __forceinline__ uint32_t swz4(int e0, int j)
+{
+    const int R = e0 >> 5;
+    return (uint32_t)(R * 128 + ((((e0 >> 2) & 7) + j) ^ (R & 7)) * 16);
+}
+// 2-byte elements: row R = e0/64, quarter q = (e0/16)&3, chunks 2q, 2q+1.
+__device__ __forceinline__ uint32_t swz2(int e0, int j)
+{
+    const int R = e0 >> 6;
+    return (uint32_t)(R * 128 + ((((e0 >> 3) & 7) + j) ^ (R & 7)) * 16);
+}
+// Byte offset of ONE element e (any e) in a swizzled slot.
+template <int SZ>
+__device__ __forceinline__ uint32_t swz_elem(int e)
+{
+    if constexpr (SZ == 4) {
+        const int R = e >> 5;
+        return (uint32_t)(R * 128 + ((((e >> 2) & 7)) ^ (R & 7)) * 16 + (e & 3) * 4);
+    } else if constexpr (SZ == 2) {
+        const int R = e >> 6;
+        return (uint32_t)(R * 128 + ((((e >> 3) & 7)) ^ (R & 7)) * 16 + (e & 7) * 2);
+    } else {
+        return (uint32_t)e;
+    }
+}
+
+__device__ __forceinline__ void load16(const uint8_t* slot, int e0, uint32_t (&v)[16], const int32_t*)
+{
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint4 q = *reinterpret_cast<const uint4*>(slot + swz4(e0, j));
+        v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+    }
+}
+__device__ __forceinline__ void load16(const uint8_t* slot, int e0, float (&v)[16], const float*)
+{
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float4 q = *reinterpret_cast<const float4*>(slot + swz4(e0, j));
+        v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+    }
+}
+__device__ __forceinline__ void load16(const uint8_t* slot, int e0, float (&v)[16], const uint16_t*)
+{
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const uint4 q = *reinterpret_cast<const uint4*>(slot + swz2(e0, j));
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
+            v[8 * j + 2 * k] = f.x;
+            v[8 * j + 2 * k + 1] = f.y;
+        }
+    }
+}
+__device__ __forceinline__ void load16(const uint8_t* slot, int e0, uint32_t (&v)[16], const int8_t*)
+{
+    const uint4 q = *reinterpret_cast<const uint4*>(slot + e0);
+    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = (uint32_t)(int32_t)(int8_t)(w[k >> 2] >> (8 * (k & 3)));
+}
+
+template <typename A>
+__device__ __forceinline__ void store16(uint8_t* slot, int e0, const A (&o)[16])
+{
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        static_assert(sizeof(A) == 4, "4-byte outputs");
+        uint4 q;
+        q.x = *reinterpret_cast<const uint32_t*>(&o[4 * j]);
+        q.y = *reinterpret_cast<const uint32_t*>(&o[4 * j + 1]);
+        q.z = *reinterpret_cast<const uint32_t*>(&o[4 * j + 2]);
+        q.w = *reinterpret_cast<const uint32_t*>(&o[4 * j + 3]);
+        *reinterpret_cast<uint4*>(slot + swz4(e0, j)) = q;
+    }
+}
+
+// ---- TMA tensor copies -----------------------------------------------------------
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* tm, int x, int y,
+                                            uint64_t* bar, uint64_t policy)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(ptx::smem_u32(smem_dst)),
+        "l"(tm), "r"(x), "r"(y), "r"(ptx::smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, int x, int y, const void* smem_src,
+                                             uint64_t policy)
+{
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(
+                     tm),
+                 "r"(x), "r"(y), "r"(ptx::smem_u32(smem_src)), "l"(policy)
+                 : "memory");
+}
+
+template <int DT, int NC, int GPW, int NB_IN, int NB_OUT>
+__global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_constant__ McParams16 p)
+{
+    using Cfg = Mc16Cfg<DT, NC, GPW, NB_IN, NB_OUT>;
+    using Tr = Traits<DT>;
+    using In = typename Tr::In;
+    using Out = typename Tr::Out;
+    using Acc = typename Tr::Acc;
+    using Carry = typename Tr::Carry;
+    constexpr int TILE = Cfg::kTile;
+    constexpr int KC = 4;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* const smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* const in_ring = smem;
+    uint8_t* const out_ring = smem + NB_IN * Cfg::kInSlot;
+
+    __shared__ __align__(8) uint64_t in_full[NB_IN];
+    __shared__ __align__(8) uint64_t in_empty[NB_IN];
+    __shared__ __align__(8) uint64_t store_ready[NB_OUT];
+    __shared__ __align__(8) uint64_t out_empty[NB_OUT];
+    __shared__ __align__(8) uint64_t carry_ready[KC];
+    __shared__ __align__(8) uint64_t rsum_ready[2];
+    __shared__ int64_t s_store_g0[NB_OUT];
+    __shared__ Acc s_wt[2][NC];
+    __shared__ Carry s_job_sum[2][NC];
+    __shared__ Carry s_carry[KC];
+    __shared__ unsigned long long s_prof[kMcProf];
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const McGeom& gm = p.gm;
+    const int b = blockIdx.x;
+    const int64_t njobs = gm.chunks * 2;
+    const bool prof = (p.debug & 4) != 0;
+    const long long t_start = clock64();
+
+    WsHeader* hdr = reinterpret_cast<WsHeader*>(p.ws);
+    uint64_t* r_all = reinterpret_cast<uint64_t*>(p.ws + kWsDescOffset);
+    uint32_t* bar = reinterpret_cast<uint32_t*>(p.ws + kWsBarOffset);
+    const In* gin = reinterpret_cast<const In*>(p.in);
+    Out* gout = reinterpret_cast<Out*>(p.out);
+
+    if (tid < kMcProf) s_prof[tid] = 0;
+    if (tid == 0) {
+        for (int s = 0; s < NB_IN; ++s) {
+            ptx::mbar_init(&in_full[s], 1);
+            ptx::mbar_init(&in_empty[s], NC);
+        }
+        for (int o = 0; o < NB_OUT; ++o) {
+            ptx::mbar_init(&store_ready[o], NC);
+            ptx::mbar_init(&out_empty[o], 1);
+        }
+        for (int k = 0; k < KC; ++k) ptx::mbar_init(&carry_ready[k], 1);
+        for (int k = 0; k < 2; ++k) ptx::mbar_init(&rsum_ready[k], NC);
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+
+    auto block_range = [&](int64_t c, int64_t& lo, int64_t& hi) {
+        lo = c * gm.chunk + (int64_t)b * gm.block;
+        hi = lo + gm.block;
+        if (lo > gm.n) lo = gm.n;
+        if (hi > gm.n) hi = gm.n;
+    };
+
+    if (warp == 0) {
+        // =========================== producer ===========================
+        if (lane == 0) {
+            const uint64_t pol_keep = ptx::policy_evict_last();
+            const uint64_t pol_drop = ptx::policy_evict_first();
+            int64_t q_tile = 0;
+            for (int64_t q = 0; q < njobs; ++q) {
+                int64_t c;
+                bool is_scan;
+                mc_job(q, gm.chunks, c, is_scan);
+                int64_t lo, hi;
+                block_range(c, lo, hi);
+                for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++q_tile) {
+                    const int s = (int)(q_tile % NB_IN);
+                    const uint32_t use = (uint32_t)(q_tile / NB_IN);
+                    if (use > 0) mbar_wait_prof(&in_empty[s], (use - 1) & 1u, prof, &s_prof[0]);
+                    uint8_t* dst = in_ring + s * Cfg::kInSlot;
+                    const uint64_t pol = is_scan ? pol_drop : pol_keep;
+                    if constexpr (sizeof(In) == 1) {
+                        int64_t m_tma = p.n_tma_in - g0;
+                        m_tma = m_tma < 0 ? 0 : (m_tma > TILE ? TILE : m_tma);
+                        if (m_tma > 0) {
+                            ptx::mbar_arrive_expect_tx(&in_full[s], (uint32_t)m_tma);
+                            ptx::tma_load_1d(dst, gin + g0, (uint32_t)m_tma, &in_full[s], pol);
+                        } else {
+                            ptx::mbar_arrive(&in_full[s]);
+                        }
+                    } else {
+                        ptx::mbar_arrive_expect_tx(&in_full[s], (uint32_t)Cfg::kInSlot);
+                        const int y0 = (int)(g0 / Cfg::kRowElemsIn);
+#pragma unroll
+                        for (int k = 0; k < Cfg::kBoxesIn; ++k)
+                            tma_load_2d(dst + k * Cfg::kBoxRowsIn * 128, &p.tm_in, 0, y0 + Cfg::kBoxRowsIn * k,
+                                        &in_full[s], pol);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // =========================== storer ===========================
+        if (lane == 0) {
+            const uint64_t pol = ptx::policy_evict_first();
+            int64_t o_tile = 0;
+            for (int64_t q = 0; q < njobs; ++q) {
+                int64_t c;
+                bool is_scan;
+                mc_job(q, gm.chunks, c, is_scan);
+                if (!is_scan) continue;
+                int64_t lo, hi;
+                block_range(c, lo, hi);
+                for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++o_tile) {
+                    const int o = (int)(o_tile % NB_OUT);
+                    mbar_wait_prof(&store_ready[o], (uint32_t)(o_tile / NB_OUT) & 1u, prof, &s_prof[5]);
+                    if (g0 < p.n_tma_out) {
+                        const int y0 = (int)(g0 / 32);
+#pragma unroll
+                        for (int k = 0; k < Cfg::kBoxesOut; ++k)
+                            tma_store_2d(&p.tm_out, 0, y0 + Cfg::kBoxRowsOut * k,
+                                         out_ring + o * Cfg::kOutSlot + k * Cfg::kBoxRowsOut * 128, pol);
+                        ptx::bulk_commit();
+                        const long long w0 = prof ? clock64() : 0;
+                        ptx::bulk_wait_read<0>();
+                        if (prof) atomicAdd(&s_prof[6], (unsigned long long)(clock64() - w0));
+                    }
+                    ptx::mbar_arrive(&out_empty[o]);
+                }
+            }
+            ptx::bulk_wait<0>();
+        }
+    } else if (warp == 2) {
+        // ========================= coordinator =========================
+        Carry chunk_carry = Carry(0);
+        if (p.carry_in != nullptr) {
+            if constexpr (Tr::kFloat)
+                chunk_carry = *reinterpret_cast<const double*>(p.carry_in);
+            else
+                chunk_carry = (uint32_t)(uint64_t)(*reinterpret_cast<const int64_t*>(p.carry_in));
+        }
+        constexpr int RPL = kMaxGridPerLane;
+        auto publish = [&](int64_t c) {
+            ptx::mbar_wait(&rsum_ready[c & 1], (uint32_t)(c >> 1) & 1u);
+            if (lane == 0) {
+                Carry t = Carry(0);
+                for (int w = 0; w < NC; ++w) t = t + s_job_sum[c & 1][w];
+                r_all[c * gm.g + b] = carry_bits(t);
+                __threadfence();
+                atomicAdd(&bar[c], 1u);
+            }
+            __syncwarp();
+        };
+        publish(0);
+        for (int64_t c = 0; c < gm.chunks; ++c) {
+            if (c + 1 < gm.chunks) publish(c + 1);
+            if (lane == 0) {
+                const long long w0 = prof ? clock64() : 0;
+                uint32_t backoff = 32;
+                while (ld_acquire_u32(&bar[c]) < (uint32_t)gm.g) {
+                    __nanosleep(backoff);
+                    backoff = backoff < 256 ? backoff * 2 : 256;
+                }
+                if (prof) s_prof[4] += (unsigned long long)(clock64() - w0);
+            }
+            __syncwarp();
+            uint64_t rb[RPL];
+#pragma unroll
+            for (int k = 0; k < RPL; ++k) {
+                const int bb = lane + 32 * k;
+                rb[k] = bb < gm.g ? ld_relaxed_u64(&r_all[c * gm.g + bb]) : 0ull;
+            }
+            Carry below = Carry(0), total = Carry(0);
+#pragma unroll
+            for (int k = 0; k < RPL; ++k) {
+                const int bb = lane + 32 * k;
+                const Carry v = bb < gm.g ? carry_from_bits<Carry>(rb[k]) : Carry(0);
+                total = total + v;
+                if (bb < b) below = below + v;
+            }
+            below = warp_reduce_fixed(below);
+            total = warp_reduce_fixed(total);
+            if (lane == 0) {
+                s_carry[c % KC] = chunk_carry + below;
+                ptx::mbar_arrive(&carry_ready[c % KC]);
+            }
+            chunk_carry = chunk_carry + total;
+        }
+    } else {
+        // =========================== compute ===========================
+        const int cw = warp - 3;
+        int64_t q_tile = 0, o_tile = 0, s_count = 0;
+
+        // 16 elements of tile-offset e0 (valid m, TMA-covered m_tma) into v.
+        auto load_lane = [&](const uint8_t* slot, int64_t g0, int e0, int m, int m_tma, Acc (&v)[16]) {
+            if (e0 + 16 <= m_tma) {
+                load16(slot, e0, v, (const In*)nullptr);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const int e = e0 + k;
+                    if (e < m_tma)
+                        v[k] = widen(*reinterpret_cast<const In*>(slot + swz_elem<sizeof(In)>(e)));
+                    else if (e < m)
+                        v[k] = widen(gin[g0 + e]);
+                    else
+                        v[k] = Acc(0);
+                }
+            }
+        };
+
+        for (int64_t q = 0; q < njobs; ++q) {
+            int64_t c;
+            bool is_scan;
+            mc_job(q, gm.chunks, c, is_scan);
+            int64_t lo, hi;
+            block_range(c, lo, hi);
+            if (!is_scan) {
+                // ---------------- Phase I: block reduction r[c][b] ----------------
+                Carry jsum = Carry(0);
+                for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++q_tile) {
+                    const int s = (int)(q_tile % NB_IN);
+                    mbar_wait_prof(&in_full[s], (uint32_t)(q_tile / NB_IN) & 1u, prof && cw == 0 && lane == 0,
+                                   &s_prof[1]);
+                    const long long tr0 = clock64();
+                    const int m = (int)(hi - g0 < TILE ? hi - g0 : TILE);
+                    int64_t mt = p.n_tma_in - g0;
+                    const int m_tma = (int)(mt < 0 ? 0 : (mt > m ? m : mt));
+                    const uint8_t* slot = in_ring + s * Cfg::kInSlot;
+#pragma unroll
+                    for (int g = 0; g < GPW; ++g) {
+                        const int e0 = (cw * GPW + g) * 512 + 16 * lane;
+                        Acc v[16];
+                        load_lane(slot, g0, e0, m, m_tma, v);
+                        // pairwise within the lane (fp32), then fp64 across tiles
+                        Acc s8[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) s8[k] = v[2 * k] + v[2 * k + 1];
+                        const Acc s4a = (s8[0] + s8[1]) + (s8[2] + s8[3]);
+                        const Acc s4b = (s8[4] + s8[5]) + (s8[6] + s8[7]);
+                        jsum = jsum + Carry(s4a + s4b);
+                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&in_empty[s]);
+                    if (prof && cw == 0 && lane == 0) {
+                        s_prof[8] += 1;
+                        s_prof[10] += (unsigned long long)(clock64() - tr0);
+                    }
+                }
+                jsum = warp_reduce_fixed(jsum);
+                if (lane == 0) {
+                    s_job_sum[c & 1][cw] = jsum;
+                    ptx::mbar_arrive(&rsum_ready[c & 1]);
+                }
+            } else {
+                // ---------------- Phase II: scan with the block carry ----------------
+                mbar_wait_prof(&carry_ready[c % KC], (uint32_t)(c / KC) & 1u, prof && cw == 0 && lane == 0,
+                               &s_prof[4]);
+                Carry carry = s_carry[c % KC];
+                for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++q_tile, ++o_tile, ++s_count) {
+                    const int s = (int)(q_tile % NB_IN);
+                    const int o = (int)(o_tile % NB_OUT);
+                    mbar_wait_prof(&in_full[s], (uint32_t)(q_tile / NB_IN) & 1u, prof && cw == 0 && lane == 0,
+                                   &s_prof[2]);
+                    const long long ts0 = clock64();
+                    const int m = (int)(hi - g0 < TILE ? hi - g0 : TILE);
+                    int64_t mt = p.n_tma_in - g0;
+                    const int m_tma = (int)(mt < 0 ? 0 : (mt > m ? m : mt));
+                    const uint8_t* slot = in_ring + s * Cfg::kInSlot;
+
+                    Acc v[GPW][16];
+                    Acc ex[GPW], gp[GPW];
+                    Acc wsum = Acc(0);
+#pragma unroll
+                    for (int g = 0; g < GPW; ++g) {
+                        const int e0 = (cw * GPW + g) * 512 + 16 * lane;
+                        load_lane(slot, g0, e0, m, m_tma, v[g]);
+#pragma unroll
+                        for (int k = 1; k < 16; ++k) v[g][k] = v[g][k - 1] + v[g][k];
+                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&in_empty[s]);
+#pragma unroll
+                    for (int g = 0; g < GPW; ++g) {
+                        const Acc incl = warp_incl_scan(v[g][15], lane);
+                        const Acc e1 = __shfl_up_sync(0xffffffffu, incl, 1);
+                        ex[g] = lane == 0 ? Acc(0) : e1;
+                        gp[g] = wsum;
+                        wsum = wsum + __shfl_sync(0xffffffffu, incl, 31);
+                    }
+                    if (lane == 0) s_wt[s_count & 1][cw] = wsum;
+                    const long long ts1 = clock64();
+                    named_bar_sync(1, NC * 32);
+                    const long long ts2 = clock64();
+                    const Acc x = lane < NC ? s_wt[s_count & 1][lane] : Acc(0);
+                    const Acc xi = warp_incl_scan(x, lane);
+                    const Acc xe = __shfl_up_sync(0xffffffffu, xi, 1);
+                    const Acc wpref = __shfl_sync(0xffffffffu, lane == 0 ? Acc(0) : xe, cw);
+                    const Acc agg = __shfl_sync(0xffffffffu, xi, NC - 1);
+
+                    if (o_tile >= NB_OUT)
+                        mbar_wait_prof(&out_empty[o], (uint32_t)(o_tile / NB_OUT - 1) & 1u,
+                                       prof && cw == 0 && lane == 0, &s_prof[3]);
+                    uint8_t* ost = out_ring + o * Cfg::kOutSlot;
+#pragma unroll
+                    for (int g = 0; g < GPW; ++g) {
+                        const int e0 = (cw * GPW + g) * 512 + 16 * lane;
+                        Acc B;
+                        if constexpr (Tr::kFloat)
+                            B = (float)(carry + (double)((wpref + gp[g]) + ex[g]));
+                        else
+                            B = carry + wpref + gp[g] + ex[g];
+                        Acc o16[16];
+                        if (p.exclusive) {
+                            o16[0] = B;
+#pragma unroll
+                            for (int k = 1; k < 16; ++k) o16[k] = B + v[g][k - 1];
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) o16[k] = B + v[g][k];
+                        }
+                        if (g0 + e0 + 16 <= p.n_tma_out) {
+                            store16(ost, e0, o16);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) {
+                                const int64_t gi = g0 + e0 + k;
+                                if (gi < p.n_tma_out)
+                                    *reinterpret_cast<Acc*>(ost + swz_elem<4>(e0 + k)) = o16[k];
+                                else if (e0 + k < m)
+                                    gout[gi] = narrow(o16[k], (Out*)nullptr);
+                            }
+                        }
+                    }
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (cw == 0) s_store_g0[o] = g0;
+                        ptx::mbar_arrive(&store_ready[o]);
+                    }
+                    carry = carry + Carry(agg);
+                    if (prof && cw == 0 && lane == 0) {
+                        s_prof[9] += 1;
+                        s_prof[11] += (unsigned long long)(ts1 - ts0);
+                        s_prof[12] += (unsigned long long)(ts2 - ts1);
+                        s_prof[13] += (unsigned long long)(clock64() - ts2);
+                    }
+                }
+            }
+        }
+    }
+
+    __syncthreads();
+    if (prof && tid == 0) s_prof[7] = (unsigned long long)(clock64() - t_start);
+    __syncthreads();
+    if (prof && tid < kMcProf && (blockIdx.x + 1) * kMcProf * 8 <= (int)(kWsBarOffset - kWsPartialsOffset))
+        reinterpret_cast<unsigned long long*>(p.ws + kWsPartialsOffset)[blockIdx.x * kMcProf + tid] = s_prof[tid];
+    if (tid == 0) {
+        __threadfence();
+        const uint32_t prev = atomicAdd(&hdr->done, 1u);
+        if (prev == gridDim.x - 1) {
+            // every CTA is past every barrier: reset the counters for the next call
+            for (int64_t c = 0; c < gm.chunks; ++c) bar[c] = 0;
+            hdr->done = 0;
+            __threadfence();
+        }
+    }
+}
+
+}  // namespace scan

@@ -1,15 +1,19 @@
 // scan_api.cu -- the C ABI declared in include/scan.h: argument checks,
 // path selection and kernel launches.  All arithmetic is in
 // scan_kernels.cuh; nothing here touches element data.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include <atomic>
 #include <mutex>
 
 #include "../../include/scan.h"
 #include "scan_kernels.cuh"
+#include "scan_ws.cuh"
+#include "mcscan.cuh"
 
 using namespace scan;
 
@@ -54,6 +58,15 @@ size_t out_size(int) { return 4; }
 bool is_float(int dt) { return dt == SCAN_F32_F32 || dt == SCAN_F16_F32; }
 size_t desc_bytes(int dt) { return is_float(dt) ? 32 : 16; }
 
+int debug_bits()
+{
+    static int v = [] {
+        const char* e = getenv("SCAN_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 int variant()
 {
     static int v = [] {
@@ -90,6 +103,7 @@ struct Variant {
         p.tiles_per_seg = (p.seg_len + kTile - 1) / kTile;
         p.num_tiles = p.tiles_per_seg * p.num_segs;
         p.static_sched = p.tiles_per_seg == 1;
+        p.debug = debug_bits();
         int64_t grid = (int64_t)di.sms * occ;
         if (grid > p.num_tiles) grid = p.num_tiles;
         k_scan_tiles<DT, TH, RW, ST, OS, MB><<<(unsigned)grid, TH, kSmem, s>>>(p);
@@ -98,40 +112,238 @@ struct Variant {
     }
 };
 
-// Tuned per dtype; SCAN_VARIANT selects alternatives.
+// Warp-specialized multi-tile kernel (scan_ws.cuh): one CTA per SM.
+template <int DT, int NC, int NL, int RW, int NBI, int NBO>
+struct WsVariant {
+    using Cfg = WsCfg<DT, NC, NL, RW, NBI, NBO>;
+    static constexpr int kTile = Cfg::kTile;
+
+    static int ready()
+    {
+        static std::once_flag once;
+        static cudaError_t err = cudaSuccess;
+        std::call_once(once, [] {
+            err = cudaFuncSetAttribute(k_scan_ws<DT, NC, NL, RW, NBI, NBO>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+        });
+        return err == cudaSuccess;
+    }
+
+    static int launch(ScanParams p, cudaStream_t s, const DevInfo& di)
+    {
+        if (!ready()) return SCAN_ERR_CUDA;
+        p.tiles_per_seg = (p.seg_len + kTile - 1) / kTile;
+        p.num_tiles = p.tiles_per_seg * p.num_segs;
+        p.static_sched = 0;
+        p.debug = debug_bits();
+        int64_t grid = di.sms;
+        if (grid > p.num_tiles) grid = p.num_tiles;
+        k_scan_ws<DT, NC, NL, RW, NBI, NBO><<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(p);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+    }
+};
+
+// Persistent cooperative MCScan with L2 splitting (mcscan.cuh): 1-D scans.
+int env_int(const char* name, int dflt)
+{
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+constexpr int kMaxGrid = 192;  // workspace sizing bound on the CTA count (B200: 148)
+constexpr int64_t kMcMinElems = 1 << 20;  // below this the look-back kernel wins (one chunk)
+
+// ---- TMA tensor maps (driver entry point, no libcuda link dependency) ----------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn()
+{
+    static EncodeTiledFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (EncodeTiledFn) nullptr;
+        return (EncodeTiledFn)f;
+    }();
+    return fn;
+}
+
+// [rows x 128 B] view of a 16-byte-aligned array, 256-row boxes, 128 B swizzle.
+bool encode_rows128(CUtensorMap* tm, const void* base, int64_t rows, int elem_bytes, int box_rows)
+{
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || rows < 1) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)(128 / elem_bytes), (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {(cuuint32_t)(128 / elem_bytes), (cuuint32_t)box_rows};
+    const cuuint32_t es[2] = {1, 1};
+    const CUtensorMapDataType dt = elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+    return fn(tm, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Second-generation MCScan: 16 contiguous elements per lane (mcscan16.cuh).
+template <int DT, int NC, int GPW, int NBI, int NBO>
+struct Mc16Variant {
+    using Cfg = Mc16Cfg<DT, NC, GPW, NBI, NBO>;
+    static constexpr int kTile = Cfg::kTile;
+
+    static int launch(const ScanParams& sp, cudaStream_t s, const DevInfo& di, int bt)
+    {
+        using In = typename Traits<DT>::In;
+        static std::once_flag once;
+        static cudaError_t err = cudaSuccess;
+        std::call_once(once, [] {
+            err = cudaFuncSetAttribute(k_mcscan16<DT, NC, GPW, NBI, NBO>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+        });
+        if (err != cudaSuccess) return SCAN_ERR_CUDA;
+        McParams16 p;
+        memset(&p, 0, sizeof(p));
+        const int64_t n = sp.seg_len;
+        const int64_t rows_out = n / 32;
+        if (!encode_rows128(&p.tm_out, sp.out, rows_out, 4, Cfg::kBoxRowsOut)) return SCAN_ERR_CUDA;
+        if constexpr (sizeof(In) == 1) {
+            p.n_tma_in = n & ~(int64_t)15;
+        } else {
+            const int64_t rows_in = n / Cfg::kRowElemsIn;
+            if (!encode_rows128(&p.tm_in, sp.in, rows_in, (int)sizeof(In), Cfg::kBoxRowsIn)) return SCAN_ERR_CUDA;
+            p.n_tma_in = rows_in * Cfg::kRowElemsIn;
+        }
+        p.n_tma_out = rows_out * 32;
+        p.in = sp.in;
+        p.out = sp.out;
+        p.carry_in = sp.carry_in;
+        p.ws = sp.ws;
+        p.exclusive = sp.exclusive;
+        p.debug = debug_bits();
+        p.gm.n = n;
+        p.gm.tile = kTile;
+        p.gm.g = di.sms < kMaxGrid ? di.sms : kMaxGrid;
+        const int64_t per_cta = (n + (int64_t)p.gm.g * kTile - 1) / ((int64_t)p.gm.g * kTile);
+        p.gm.bt = bt < per_cta ? bt : (per_cta < 1 ? 1 : per_cta);
+        p.gm.block = p.gm.bt * kTile;
+        p.gm.chunk = p.gm.block * p.gm.g;
+        p.gm.chunks = (n + p.gm.chunk - 1) / p.gm.chunk;
+        if (p.gm.chunks > kMaxChunks) {  // larger blocks so the counters fit
+            p.gm.bt = (n + (int64_t)kMaxChunks * p.gm.g * kTile - 1) / ((int64_t)kMaxChunks * p.gm.g * kTile);
+            p.gm.block = p.gm.bt * kTile;
+            p.gm.chunk = p.gm.block * p.gm.g;
+            p.gm.chunks = (n + p.gm.chunk - 1) / p.gm.chunk;
+        }
+        void* args[] = {&p};
+        cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_mcscan16<DT, NC, GPW, NBI, NBO>,
+                                                    dim3(p.gm.g), dim3(Cfg::kThreads), args, Cfg::kSmem, s);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return e == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+    }
+};
+
+// Workspace bytes the MCScan path needs for n elements (tile >= 8192, bt >= 1):
+// r[c][b] (8 B) per block; barrier counters live in the fixed header region.
+size_t mc_workspace_bytes(int64_t n)
+{
+    const int64_t blocks = (n + 8191) / 8192 + kMaxGrid;  // r[c][b] entries, upper bound
+    return kWsDescOffset + (size_t)blocks * 8 + 64;
+}
+
+// Chunk = G blocks of bt tiles; ~16 MB of input per chunk keeps two chunks'
+// inputs resident in the 126 MB L2 next to the streaming outputs.
+template <typename V, int DT>
+int launch_mc_sized(const ScanParams& p, cudaStream_t s, const DevInfo& di)
+{
+    using In = typename Traits<DT>::In;
+    const int64_t tile_bytes = (int64_t)V::kTile * (int64_t)sizeof(In);
+    const int64_t want = (int64_t)env_int("SCAN_MC_CHUNK_MB", 16) << 20;
+    int64_t bt = (want + di.sms * tile_bytes / 2) / (di.sms * tile_bytes);
+    bt = bt < 1 ? 1 : bt;
+    return V::launch(p, s, di, env_int("SCAN_MC_BT", (int)bt));
+}
+
 template <int DT>
-int launch_dt(ScanParams p, cudaStream_t s, const DevInfo& di, int64_t& tile)
+int launch_mc(const ScanParams& p, cudaStream_t s, const DevInfo& di)
 {
     constexpr bool wide_in = (DT == SCAN_I32_I32 || DT == SCAN_F32_F32);
-    switch (variant()) {
-    case 1:
-        tile = Variant<DT, 256, 8, 2, 1, 2>::kTile;
-        return Variant<DT, 256, 8, 2, 1, 2>::launch(p, s, di);
-    case 2:
-        tile = Variant<DT, 512, 4, 3, 2, 1>::kTile;
-        return Variant<DT, 512, 4, 3, 2, 1>::launch(p, s, di);
-    case 3:
-        tile = Variant<DT, 256, 4, 3, 2, 3>::kTile;
-        return Variant<DT, 256, 4, 3, 2, 3>::launch(p, s, di);
+    switch (env_int("SCAN_MC", 0)) {
+    case 0:
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 2, 2, 1>, DT>(p, s, di);
+        else if constexpr (DT == SCAN_F16_F32) return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 2>, DT>(p, s, di);
+        else return launch_mc_sized<Mc16Variant<DT, 16, 2, 4, 2>, DT>(p, s, di);
+    case 4:
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 1, 4, 2>, DT>(p, s, di);
+        else return launch_mc_sized<Mc16Variant<DT, 16, 1, 4, 3>, DT>(p, s, di);
+    case 5:
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 8, 4, 2, 1>, DT>(p, s, di);
+        else return launch_mc_sized<Mc16Variant<DT, 8, 4, 3, 2>, DT>(p, s, di);
     default:
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 2, 2, 1>, DT>(p, s, di);
+        else if constexpr (DT == SCAN_F16_F32) return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 2>, DT>(p, s, di);
+        else return launch_mc_sized<Mc16Variant<DT, 16, 2, 4, 2>, DT>(p, s, di);
+    }
+}
+
+// Single-tile-per-segment (static) and tuning-alternative kernels; the default
+// path for multi-tile segments is the warp-specialized kernel.  SCAN_VARIANT
+// selects alternatives for experiments.
+template <int DT>
+int launch_dt(ScanParams p, cudaStream_t s, const DevInfo& di)
+{
+    constexpr bool wide_in = (DT == SCAN_I32_I32 || DT == SCAN_F32_F32);
+    using Small = Variant<DT, 512, 4, 2, 1, 2>;  // 8192-element tiles
+    const int v = variant();
+    if (v == 0 || p.seg_len <= Small::kTile) {
+        if (p.seg_len <= Small::kTile) return Small::launch(p, s, di);
+        if (p.num_segs == 1 && p.tma_in && p.tma_out && p.seg_len >= kMcMinElems &&
+            env_int("SCAN_NO_MC", 0) == 0)
+            return launch_mc<DT>(p, s, di);
         if constexpr (wide_in) {
-            tile = Variant<DT, 512, 4, 2, 1, 2>::kTile;
-            return Variant<DT, 512, 4, 2, 1, 2>::launch(p, s, di);
+            return WsVariant<DT, 16, 3, 8, 3, 3>::launch(p, s, di);
+        } else if constexpr (DT == SCAN_F16_F32) {
+            return WsVariant<DT, 16, 3, 4, 4, 3>::launch(p, s, di);
         } else {
-            tile = Variant<DT, 512, 4, 3, 1, 2>::kTile;
-            return Variant<DT, 512, 4, 3, 1, 2>::launch(p, s, di);
+            return WsVariant<DT, 16, 2, 8, 3, 2>::launch(p, s, di);
         }
     }
+#define SCAN_VARIANT_CASE(ID, TH, RW, ST, OS, MB) \
+    case ID: return Variant<DT, TH, RW, ST, OS, MB>::launch(p, s, di);
+    switch (v) {
+        SCAN_VARIANT_CASE(1, 256, 8, 2, 1, 2)
+        SCAN_VARIANT_CASE(2, 512, 4, 1, 1, 2)
+        SCAN_VARIANT_CASE(4, 256, 8, 1, 1, 2)
+        SCAN_VARIANT_CASE(5, 128, 8, 1, 1, 6)
+    case 10:
+        if constexpr (wide_in) return WsVariant<DT, 16, 1, 8, 3, 3>::launch(p, s, di);
+        else return WsVariant<DT, 16, 1, 8, 3, 2>::launch(p, s, di);
+    case 11:
+        if constexpr (wide_in) return WsVariant<DT, 16, 2, 4, 6, 6>::launch(p, s, di);
+        else return WsVariant<DT, 16, 2, 4, 4, 4>::launch(p, s, di);
+    case 12:
+        if constexpr (wide_in) return WsVariant<DT, 16, 3, 4, 6, 6>::launch(p, s, di);
+        else return WsVariant<DT, 16, 3, 4, 4, 3>::launch(p, s, di);
+    case 14:
+        if constexpr (wide_in) return WsVariant<DT, 16, 2, 8, 2, 2>::launch(p, s, di);
+        else return WsVariant<DT, 16, 2, 8, 3, 2>::launch(p, s, di);
+    case 13:
+        if constexpr (wide_in) return WsVariant<DT, 16, 6, 4, 6, 6>::launch(p, s, di);
+        else return WsVariant<DT, 16, 4, 4, 4, 4>::launch(p, s, di);
+    default:
+        return Small::launch(p, s, di);
+    }
+#undef SCAN_VARIANT_CASE
 }
 
 int launch_any(int dt, ScanParams p, cudaStream_t s, const DevInfo& di)
 {
-    int64_t tile = 0;
     switch (dt) {
-    case SCAN_I32_I32: return launch_dt<0>(p, s, di, tile);
-    case SCAN_F32_F32: return launch_dt<1>(p, s, di, tile);
-    case SCAN_F16_F32: return launch_dt<2>(p, s, di, tile);
-    case SCAN_I8_I32: return launch_dt<3>(p, s, di, tile);
+    case SCAN_I32_I32: return launch_dt<0>(p, s, di);
+    case SCAN_F32_F32: return launch_dt<1>(p, s, di);
+    case SCAN_F16_F32: return launch_dt<2>(p, s, di);
+    case SCAN_I8_I32: return launch_dt<3>(p, s, di);
     }
     return SCAN_ERR_ARG;
 }
@@ -203,7 +415,9 @@ const char* scan_status_string(int status)
 size_t scan_workspace_bytes(int dtype, int64_t n)
 {
     if (!valid_dt(dtype) || n < 0) return 0;
-    return kWsDescOffset + (size_t)tiles_for(n) * desc_bytes(dtype);
+    const size_t lb = kWsDescOffset + (size_t)tiles_for(n) * desc_bytes(dtype);
+    const size_t mc = mc_workspace_bytes(n);
+    return lb > mc ? lb : mc;
 }
 
 size_t scan_rows_workspace_bytes(int dtype, int64_t rows, int64_t cols)

@@ -49,8 +49,11 @@ namespace scan {
 // ---------------------------------------------------------------- workspace
 constexpr uint32_t kWsMagic = 0x5CA7B200u;
 constexpr size_t kWsPartialsOffset = 256;         // scan_total per-CTA partials
-constexpr int kMaxTotalCtas = 2048;
-constexpr size_t kWsDescOffset = kWsPartialsOffset + 8 * kMaxTotalCtas;  // 16640
+constexpr int kMaxTotalCtas = 4096;
+constexpr int kMaxGridPerLane = 6;   // k_mcscan coordinator: up to 192 CTAs
+constexpr size_t kWsBarOffset = kWsPartialsOffset + 8 * kMaxTotalCtas;   // 33024: MCScan barriers
+constexpr int kMaxChunks = 8192;                                            // u32 counter per chunk
+constexpr size_t kWsDescOffset = kWsBarOffset + 4 * kMaxChunks;            // 65792
 
 struct WsHeader {
     uint32_t magic;
@@ -162,6 +165,30 @@ __device__ __forceinline__ double warp_sum(double x)
     return x;
 }
 
+// Butterfly reduction over the warp (fixed order: every lane gets the same bits).
+template <typename T>
+__device__ __forceinline__ T warp_reduce_fixed(T x)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = x + __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// Carry <-> 64-bit storage word.
+__device__ __forceinline__ uint64_t carry_bits(uint32_t v) { return v; }
+__device__ __forceinline__ uint64_t carry_bits(double v) { return (uint64_t)__double_as_longlong(v); }
+template <typename C>
+__device__ __forceinline__ C carry_from_bits(uint64_t b);
+template <>
+__device__ __forceinline__ uint32_t carry_from_bits<uint32_t>(uint64_t b) { return (uint32_t)b; }
+template <>
+__device__ __forceinline__ double carry_from_bits<double>(uint64_t b) { return __longlong_as_double((long long)b); }
+
+using ptx::ld_acquire_u32;
+using ptx::ld_acquire_u64;
+using ptx::ld_relaxed_u64;
+using ptx::named_bar_sync;
+
 // ---- look-back descriptors -------------------------------------------------
 // int: 2 slots per tile {aggregate, inclusive}; fp64: 4 slots {agg hi, agg lo,
 // incl hi, incl lo}.  Slot = (epoch << 32) | payload.
@@ -216,39 +243,110 @@ struct Desc<double> {
     }
 };
 
-// Warp-cooperative decoupled look-back for tile t of a segment whose first
-// tile is seg_first.  Returns the exclusive prefix of the tile (carry_seg +
-// all aggregates of tiles seg_first..t-1).  All 32 lanes call it.
-template <typename Carry>
-__device__ __forceinline__ Carry lookback(const uint64_t* desc, int64_t t, int64_t seg_first,
-                                          Carry carry_seg, uint32_t tag, int lane)
+// Warp-cooperative decoupled look-back for tile t.  `lo` < t is a tile whose
+// inclusive prefix `lo_val` is already known to the caller: either the CTA's
+// own previously processed tile (tiles are claimed in increasing order, so it
+// is always below t) or the virtual tile before the segment (value = the
+// segment's carry-in).  The warp therefore only has to sum the aggregates of
+// tiles lo+1..t-1, stopping early at the nearest inclusive prefix.  Each lane
+// reads BATCH descriptors per round (idx = hi - lane - 32 r), so one L2 round
+// trip covers 32*BATCH predecessors instead of 32.
+template <typename Carry, int BATCH>
+__device__ __forceinline__ Carry lookback(const uint64_t* desc, int64_t t, int64_t lo, Carry lo_val,
+                                          uint32_t tag, int lane, uint32_t backoff,
+                                          unsigned long long* stats = nullptr)
 {
     using D = Desc<Carry>;
-    Carry excl = Carry(0);
-    int64_t pred = t - 1;
-    uint32_t backoff = 32;
+    Carry acc = Carry(0);
+    int64_t hi = t - 1;  // highest tile not yet accounted for
     while (true) {
-        int64_t idx = pred - lane;
-        int st;
-        Carry v;
-        if (idx >= seg_first) {
-            st = D::read(desc + idx * D::kSlots, tag, v);
-        } else {
-            st = 2;  // the virtual tile before the segment holds the carry-in
-            v = (idx == seg_first - 1) ? carry_seg : Carry(0);
+        int st[BATCH];
+        Carry v[BATCH];
+#pragma unroll
+        for (int r = 0; r < BATCH; ++r) {
+            int64_t idx = hi - lane - 32 * r;
+            if (idx > lo) {
+                st[r] = D::read(desc + idx * D::kSlots, tag, v[r]);
+            } else {
+                st[r] = 2;
+                v[r] = (idx == lo) ? lo_val : Carry(0);
+            }
         }
-        uint32_t pm = __ballot_sync(0xffffffffu, st == 2);
-        uint32_t xm = __ballot_sync(0xffffffffu, st == 0);
-        uint32_t need = pm ? ((pm & (0u - pm)) << 1) - 1u : 0xffffffffu;  // lanes 0..first P
-        if (xm & need) {
+        bool progressed = false;
+        if (stats && lane == 0) atomicAdd(&stats[0], 1ull);  // rounds
+#pragma unroll
+        for (int r = 0; r < BATCH; ++r) {
+            uint32_t pm = __ballot_sync(0xffffffffu, st[r] == 2);
+            uint32_t xm = __ballot_sync(0xffffffffu, st[r] == 0);
+            uint32_t need = pm ? ((pm & (0u - pm)) << 1) - 1u : 0xffffffffu;  // lanes 0..first P
+            if (xm & need) break;  // a needed predecessor has not published yet
+            Carry c = ((need >> lane) & 1u) ? v[r] : Carry(0);
+            acc = acc + warp_sum(c);
+            if (stats && lane == 0) atomicAdd(&stats[7], 1ull);  // windows consumed (s_prof[11])
+            if (pm) return acc;
+            hi -= 32;
+            progressed = true;
+        }
+        if (stats && lane == 0 && !progressed) stats[1] += 1;  // stalled rounds (s_prof[5])
+        if (!progressed && backoff) {
             __nanosleep(backoff);
-            backoff = backoff < 1024 ? backoff * 2 : 1024;
-            continue;
+            backoff = backoff < 512 ? backoff * 2 : 512;
         }
-        Carry c = ((need >> lane) & 1u) ? v : Carry(0);
-        excl = excl + warp_sum(c);
-        if (pm) return excl;
-        pred -= 32;
+    }
+}
+
+// Range look-back used by the warp-specialized kernel.  Walks tiles t-1,
+// t-2, ... down to the nearest inclusive prefix (P) or to tile `lo`, which is
+// treated as a P whose value the CALLER adds afterwards (it may not be known
+// yet: `lo` is this CTA's previous tile, resolved by another look-back warp).
+// Returns the sum of the aggregates above the stop point plus, if the stop
+// was a real P, its value; *hit_lo tells whether the stop was `lo`.
+template <typename Carry, int BATCH>
+__device__ __forceinline__ Carry lookback_range(const uint64_t* desc, int64_t t, int64_t lo,
+                                                uint32_t tag, int lane, uint32_t backoff,
+                                                bool* hit_lo, unsigned long long* stats)
+{
+    using D = Desc<Carry>;
+    Carry acc = Carry(0);
+    int64_t hi = t - 1;
+    while (true) {
+        int st[BATCH];
+        Carry v[BATCH];
+#pragma unroll
+        for (int r = 0; r < BATCH; ++r) {
+            const int64_t idx = hi - lane - 32 * r;
+            st[r] = 2;
+            v[r] = Carry(0);
+            if (idx > lo) st[r] = D::read(desc + idx * D::kSlots, tag, v[r]);
+        }
+        if (stats && lane == 0) atomicAdd(&stats[0], 1ull);
+        int consumed = 0;
+        bool blocked = false;
+#pragma unroll
+        for (int r = 0; r < BATCH; ++r) {
+            if (blocked) continue;
+            const uint32_t pm = __ballot_sync(0xffffffffu, st[r] == 2);
+            const uint32_t xm = __ballot_sync(0xffffffffu, st[r] == 0);
+            const uint32_t need = pm ? ((pm & (0u - pm)) << 1) - 1u : 0xffffffffu;
+            if (xm & need) {  // a needed predecessor has not published yet
+                blocked = true;
+                continue;
+            }
+            const Carry c = ((need >> lane) & 1u) ? v[r] : Carry(0);
+            acc = acc + warp_sum(c);
+            if (stats && lane == 0) atomicAdd(&stats[7], 1ull);
+            if (pm) {
+                const int64_t stop = hi - 32 * r - (__ffs(pm) - 1);
+                *hit_lo = stop <= lo;
+                return acc;
+            }
+            ++consumed;
+        }
+        hi -= 32 * consumed;
+        if (consumed == 0) {
+            if (stats && lane == 0) atomicAdd(&stats[1], 1ull);
+            if (backoff) __nanosleep(backoff);
+        }
     }
 }
 
@@ -268,6 +366,8 @@ struct ScanParams {
     int tma_in;             // segment bases and strides 16-byte aligned (input)
     int tma_out;            // same for output
     int static_sched;       // one tile per segment: no tickets, no look-back
+    int debug;              // bit 0: skip look-back (timing only; wrong results); bit 1: spin without
+                            // nanosleep; bit 2: per-CTA stall counters into the workspace
 };
 
 template <int THREADS, int ROWS>
@@ -321,15 +421,16 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
     const In* gin = reinterpret_cast<const In*>(p.in);
     Out* gout = reinterpret_cast<Out*>(p.out);
 
-    uint64_t pol_in = 0, pol_out = 0;
-    int64_t static_next = blockIdx.x;
+    const uint64_t pol_in = ptx::policy_evict_first();
+    const uint64_t pol_out = ptx::policy_evict_first();
 
-    // Claim the next tile and, if it can go by TMA, start streaming it into stage s.
-    auto issue = [&](int s) {
+    // Claim this CTA's q-th tile and, if it can go by TMA, start streaming it
+    // into stage s.  Called by one thread (tid 0 in the prologue, tid 32 --
+    // warp 1, so the look-back warp never waits on the ticket atomic -- later).
+    auto issue = [&](int s, int64_t q) {
         int64_t t;
         if (p.static_sched) {
-            t = static_next;
-            static_next += gridDim.x;
+            t = (int64_t)blockIdx.x + q * gridDim.x;
         } else {
             t = (int64_t)atomicAdd(&hdr->ticket, 1u);
         }
@@ -356,17 +457,17 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
             if (hdr->magic != kWsMagic) hdr->error = 1;
             s_epoch = hdr->epoch;
         }
-        pol_in = ptx::policy_evict_first();
-        pol_out = ptx::policy_evict_first();
         for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&full_bar[s], 1);
         ptx::fence_mbar_init();
-        for (int s = 0; s < STAGES; ++s) issue(s);
+        for (int s = 0; s < STAGES; ++s) issue(s, s);
     }
     __syncthreads();
     const uint32_t tag = s_epoch;
 
     uint32_t phases = 0;  // bit s = parity of the next wait on full_bar[s]
     int ostage = 0;
+    int64_t last_t = -1;       // warp 0: this CTA's previous tile and its inclusive prefix
+    Carry last_incl = Carry(0);
     for (int64_t iter = 0;; ++iter) {
         const int s = (int)(iter % STAGES);
         const int64_t t = s_ticket[s];
@@ -429,8 +530,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
         if (lane == 0) s_warp_tot[warp] = wsum;
         __syncthreads();  // [A] stage s fully read; warp totals visible
 
-        // Refill stage s with the next claimed tile while we finish this one.
-        if (tid == 0) issue(s);
+        // STAGES > 1: refill stage s with the next claimed tile while we finish
+        // this one.  (That tile's aggregate then waits for this tile's
+        // look-back: a chain.  STAGES == 1 claims after the look-back instead.)
+        if (STAGES > 1 && tid == 32) issue(s, iter + STAGES);
 
         // ---- a4: block scan of warp totals + decoupled look-back (warp 0)
         if (warp == 0) {
@@ -455,17 +558,31 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
             } else {
                 if (lane == 0)
                     Desc<Carry>::publish(desc + t * Desc<Carry>::kSlots, false, tag, Carry(agg));
-                prefix = lookback<Carry>(desc, t, t - k, carry_seg, tag, lane);
+                const int64_t seg_first = t - k;
+                const bool own = last_t >= seg_first;
+                if (p.debug & 1)
+                    prefix = Carry(0);
+                else
+                    prefix = lookback<Carry, 8>(desc, t, own ? last_t : seg_first - 1,
+                                                own ? last_incl : carry_seg, tag, lane,
+                                                (p.debug & 2) ? 0u : 32u);
                 if (lane == 0 && k + 1 < p.tiles_per_seg)
                     Desc<Carry>::publish(desc + t * Desc<Carry>::kSlots, true, tag,
                                          prefix + Carry(agg));
             }
+            last_t = t;
+            last_incl = prefix + Carry(agg);
             if (lane == 0) s_prefix = prefix;
         }
         // The output staging buffer we are about to fill must no longer be
         // read by the bulk store issued OSTAGES tiles ago.
         if (tid == 0 && p.tma_out) ptx::bulk_wait_read<OSTAGES - 1>();
         __syncthreads();  // [B] prefix and warp prefixes visible
+
+        // STAGES == 1: claim the next tile only now, when this CTA is free to
+        // process it right after its data lands, so its aggregate is published
+        // one load latency after the claim, independent of any look-back.
+        if (STAGES == 1 && tid == 32) issue(0, iter + 1);
 
         // ---- a5: epilogue
         const Carry P = s_prefix;

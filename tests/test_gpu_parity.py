@@ -221,3 +221,32 @@ def test_total_and_carry(cuda, oracle, inputs_mod, dt):
     for r in range(G):
         c = cuda.carry_from_totals(totals, r, TORCH_IN[dt])
         assert c.item() == sum([3, -7, 11, 100, 5][:r])
+
+
+# ---------------------------------------------- large 1-D (MCScan + L2 split)
+
+LARGE = [(1 << 20) + 1, (1 << 20) + 17, (1 << 20) + 31, 3 * (1 << 20) + 5, (1 << 22) + 7,
+         (1 << 24) + 13, 5 * (1 << 22) + 100003]
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+def test_large_ragged(cuda, oracle, inputs_mod, dt):
+    """Multi-chunk arrays whose length is not a multiple of the 128-byte TMA
+    row, of the tile or of the chunk: exercises the chunk barrier, the block
+    carries and the directly loaded/stored tail."""
+    for i, n in enumerate(LARGE):
+        x = host_input(inputs_mod, dt, n, seed=1000 + i)
+        exclusive = bool(i % 2)
+        carry = None
+        c = None
+        if i % 3 == 2:
+            if dt in ("i32", "i8"):
+                c = 123456789012
+                carry = torch.tensor([c], dtype=torch.int64, device="cuda")
+            else:
+                c = -777.25
+                carry = torch.tensor([c], dtype=torch.float64, device="cuda")
+        fn = cuda.exclusive if exclusive else cuda.inclusive
+        got = fn(to_dev(x, dt), carry_in=carry)
+        torch.cuda.synchronize()
+        assert_parity(oracle, got, oracle_1d(oracle, x, dt, exclusive, carry=c), dt)
