@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""bench.py -- device-wide prefix sum on B200: the BASELINE.json metric
+"scan GB/s (in+out bytes) and % of HBM peak, at 1/2/4/8 B200".
+
+Default workload (config.workload): C5 of BASELINE.json -- fp32 inclusive scan
+of n = 2^32 N(0,1) values (16 GiB in, 16 GiB out), the config the metric is
+quoted on at 1/2/4/8 GPUs that fits one GPU.  At N > 1 the array is sharded
+contiguously across ranks (strong scaling: n fixed) and each step is the
+device-level Reduce-Scan-Scan of paper_2505_15112_b200.dist (scan_total ->
+NCCL all-gather of the shard totals -> carry -> shard scan).  --config selects
+C1..C5 for other measurements; the driver's line is the default.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+
+One JSON line on stdout (rank 0).  Timing: W untimed warm-up steps, then K
+steps between barrier + cuda.synchronize, CUDA events on the launching stream,
+max over ranks.  Inputs (>= 512 MiB) exceed the 126 MB L2, so no flush.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "scan GB/s (in+out bytes) and % of HBM peak, at 1/2/4/8 B200"
+
+# Per config: input recipe, bytes per element in+out, scan op, shardable.
+WORK = {
+    "C1": dict(name="C1 int32 inclusive+exclusive, n=65,536, U[-100,100], seed 0", dt="i32",
+               n=65536, rows=1, ops=("inclusive", "exclusive"), bpe=8, shard=False, dtype="int32"),
+    "C2": dict(name="C2 fp16->fp32 inclusive, n=2^28, U[0,1) rounded to fp16, seed 1", dt="f16",
+               n=1 << 28, rows=1, ops=("inclusive",), bpe=6, shard=False, dtype="f32"),
+    "C3": dict(name="C3 int8 flags->int32 exclusive, n=2^30, Bernoulli(0.5), seed 2", dt="i8",
+               n=1 << 30, rows=1, ops=("exclusive",), bpe=5, shard=True, dtype="int32"),
+    "C4": dict(name="C4 fp32 row scan 4096x131072, softmax(4*N(0,1)) rows, seed 3", dt="f32",
+               n=131072, rows=4096, ops=("rows",), bpe=8, shard=False, dtype="f32"),
+    "C5": dict(name="C5 fp32 inclusive, n=2^32, N(0,1), seed 4", dt="f32", n=1 << 32, rows=1,
+               ops=("inclusive",), bpe=8, shard=True, dtype="f32"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy_ of 1 Gi bf16)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def recorded_traffic(cfg: str):
+    """DRAM bytes per launch of the dominant kernel from a committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d.get(cfg)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------- inputs
+def make_input(cfg, lo, count, device):
+    import torch
+
+    import inputs
+    c = inputs.CONFIGS[cfg]
+    if c["kind"] == inputs.F32_SOFTMAX:
+        x = torch.empty((count, c["n"]), dtype=torch.float32, device=device)
+        inputs.fill_device(c["kind"], c["seed"], lo, count, c["n"], x)
+        return x
+    tdt = {inputs.I32_U100: torch.int32, inputs.F16_U01: torch.float16, inputs.I8_FLAG: torch.int8,
+           inputs.F32_NORMAL: torch.float32}[c["kind"]]
+    x = torch.empty(count, dtype=tdt, device=device)
+    inputs.fill_device(c["kind"], c["seed"], lo, count, 0, x)
+    return x
+
+
+# ----------------------------------------------------------------- CPU oracle
+class OracleStream:
+    """The CPU oracle, as it stands, streaming over the workload in chunks
+    (inputs generated on the host with the same recipe; generation untimed)."""
+
+    def __init__(self, cfg: str, chunk: int):
+        import inputs
+        self.cfg, self.w, self.c = cfg, WORK[cfg], inputs.CONFIGS[cfg]
+        self.chunk = chunk
+        self.pos = 0          # elements (rows for C4) consumed
+        self.states = {}
+
+    def total_units(self):
+        return self.w["rows"] if self.cfg == "C4" else self.w["n"]
+
+    def step(self):
+        """Scan the next chunk; returns (algorithmic bytes, oracle seconds)."""
+        import inputs
+        import oracle
+        w, c = self.w, self.c
+        if self.pos >= self.total_units():
+            self.pos, self.states = 0, {}
+        if self.cfg == "C4":
+            rows = max(1, min(self.chunk // w["n"], w["rows"] - self.pos))
+            X = inputs.fill_host(c["kind"], c["seed"], self.pos, rows, w["n"])
+            t0 = time.perf_counter()
+            oracle.rows(X, "f32")
+            dt = time.perf_counter() - t0
+            self.pos += rows
+            return X.size * w["bpe"], dt
+        cnt = min(self.chunk, w["n"] - self.pos)
+        x = inputs.fill_host(c["kind"], c["seed"], self.pos, cnt)
+        t0 = time.perf_counter()
+        for op in w["ops"]:
+            if w["dt"] in ("i32", "i8"):
+                st = self.states.setdefault(op, oracle.IntScan(w["dt"]))
+                st(x, op == "exclusive")
+            else:
+                st = self.states.setdefault(op, oracle.FloatScan(w["dt"]))
+                st(x, op == "exclusive", want64=False, want_abs=False, want32=True)
+        dt = time.perf_counter() - t0
+        self.pos += cnt
+        return cnt * w["bpe"] * len(w["ops"]), dt
+
+    def describe(self, units):
+        what = "rows" if self.cfg == "C4" else "elements"
+        return f"first {units} {what} of {self.total_units()} (streamed in chunks of {self.chunk})"
+
+
+def oracle_throughput(cfg: str, budget_s: float, chunk: int):
+    """cpu_baseline: oracle GB/s over the leading chunks, ~budget_s of oracle time."""
+    o = OracleStream(cfg, chunk)
+    b = t = 0.0
+    while t < budget_s and o.pos < o.total_units():
+        db, dt = o.step()
+        b += db
+        t += dt
+    return b / t / 1e9, t, o.describe(o.pos)
+
+
+def run_reference(args, rank):
+    """--impl reference: the CPU oracle as it stands, one bounded chunk per step."""
+    if rank != 0:
+        return 0
+    w = WORK[args.config]
+    chunk = w["n"] if args.config == "C1" else (1 << 24)
+    o = OracleStream(args.config, chunk)
+    for _ in range(args.warmup):
+        o.step()
+    b = t = 0.0
+    for _ in range(args.steps):
+        db, dt = o.step()
+        b += db
+        t += dt
+    value = b / t / 1e9
+    sample = f"{args.steps} steps x {chunk} {'rows-worth of elements' if args.config == 'C4' else 'elements'} " \
+             f"of the workload, single-thread C oracle (oracle/oracle_scan.c)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
+        "scaling": "strong" if w["shard"] else "weak", "vs_baseline": None, "dtype": w["dtype"],
+        "data": "synthetic (seeded counter-based generator, inputs/recipe.h)",
+        "config": {"workload": w["name"]},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2505_15112_b200 as S
+    from paper_2505_15112_b200 import dist as D
+
+    cfg = args.config
+    w = WORK[cfg]
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    S.load()
+    sharded = w["shard"] and world > 1
+    total_elems = w["n"] * w["rows"]
+    if sharded:
+        lo, hi = D.shard_bounds(w["n"], world, rank)
+        x = make_input(cfg, lo, hi - lo, dev)
+        local_elems = hi - lo
+    elif cfg == "C4":
+        x = make_input(cfg, 0, w["rows"], dev)
+        local_elems = total_elems
+    else:
+        x = make_input(cfg, 0, w["n"], dev)
+        local_elems = total_elems
+    out_dtype = torch.int32 if w["dt"] in ("i32", "i8") else torch.float32
+    out = torch.empty(x.shape, dtype=out_dtype, device=dev)
+    out2 = torch.empty_like(out) if cfg == "C1" else None
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+
+    ev_k0, ev_k1 = [], []
+
+    def scan_call(xin, o, o2=None, timed=False):
+        if timed:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        if cfg == "C4":
+            S.rows(xin, out=o)
+        elif cfg == "C1":
+            S.inclusive(xin, out=o)
+            S.exclusive(xin, out=o2)
+        elif sharded:
+            (D.sharded_exclusive if "exclusive" in w["ops"] else D.sharded_inclusive)(xin, out=o)
+        else:
+            (S.exclusive if "exclusive" in w["ops"] else S.inclusive)(xin, out=o)
+        if timed:
+            b.record(stream)
+            ev_k0.append(a)
+            ev_k1.append(b)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- warm-up + timed device region
+    for _ in range(args.warmup):
+        scan_call(x, out, out2)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    l0 = S.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        scan_call(x, out, out2, timed=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = S.launch_count() - l0
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    kernel_ms = sum(a.elapsed_time(b) for a, b in zip(ev_k0, ev_k1)) / args.steps
+    if world > 1:
+        tt = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, kernel_ms = tt.tolist()
+    ms_per_step = ms / args.steps
+    step_bytes = total_elems * w["bpe"] * (2 if cfg == "C1" else 1)
+    if not sharded and world > 1:
+        step_bytes *= world  # replicas: every rank scans the whole workload
+    value = step_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (the scan launch of each step)
+    peak, peak_src = peaks()
+    local_bytes = local_elems * w["bpe"] * (2 if cfg == "C1" else 1)
+    achieved = local_bytes / (kernel_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": recorded_traffic(cfg),
+            "peak_source": peak_src,
+            "note": "achieved = algorithmic in+out bytes of the scan launch / its CUDA-event duration"}
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, x, out, out2, scan_call, dev, stream, world, barrier, local_elems, w,
+                      step_bytes)
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, t, sample = oracle_throughput(cfg, args.cpu_seconds, 1 << 24)
+        cpu = {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
+               "sample": f"{sample}; {t:.1f} s of single-thread oracle time on the GPU box host"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "strong" if w["shard"] else "weak",
+            "vs_baseline": None, "dtype": w["dtype"],
+            "data": "synthetic (seeded counter-based generator, inputs/recipe.h; generated in HBM)",
+            "config": {
+                "workload": w["name"], "n_elements": total_elems, "bytes_per_step": step_bytes,
+                "parallelism": (f"shard{world} (contiguous shards, NCCL all-gather of shard totals)"
+                                if sharded else (f"replicas x{world}" if world > 1 else "single GPU")),
+                "pct_of_hbm_peak": round(100.0 * value / (peak * world), 2),
+                "gelem_per_s": round(total_elems * (2 if cfg == "C1" else 1) * (world if not sharded and world > 1 else 1)
+                                     / (ms_per_step * 1e-3) / 1e9, 2),
+                "l2_flush": "not needed: inputs exceed the 126 MB L2" if local_bytes > (256 << 20)
+                else "hot L2 (latency-bound size)",
+            },
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_e2e(args, x, out, out2, scan_call, dev, stream, world, barrier, local_elems, w, step_bytes):
+    """Same metric through the public API with HOST buffers: every step copies
+    the input from pinned host memory, scans, and copies the result back."""
+    import torch
+    h_in = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
+    h_in.copy_(x)
+    h_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    h_out2 = torch.empty(out.shape, dtype=out.dtype, pin_memory=True) if out2 is not None else None
+    steps = max(1, min(args.steps, args.e2e_steps))
+
+    def step():
+        x.copy_(h_in, non_blocking=True)
+        scan_call(x, out, out2)
+        h_out.copy_(out, non_blocking=True)
+        if h_out2 is not None:
+            h_out2.copy_(out2, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    barrier()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = t.item()
+    h2d = x.numel() * x.element_size()
+    d2h = out.numel() * out.element_size() * (2 if out2 is not None else 1)
+    return {"value": round(step_bytes / (ms / steps * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
+            "path": "pinned host -> cudaMemcpyAsync -> scan (C ABI) -> cudaMemcpyAsync -> pinned host"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(WORK), default="C5")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (contract minimum)")
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

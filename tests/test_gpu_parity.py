@@ -250,3 +250,34 @@ def test_large_ragged(cuda, oracle, inputs_mod, dt):
         got = fn(to_dev(x, dt), carry_in=carry)
         torch.cuda.synchronize()
         assert_parity(oracle, got, oracle_1d(oracle, x, dt, exclusive, carry=c), dt)
+
+
+@pytest.mark.parametrize("dt", ["i8", "f32", "i32"])
+def test_sharded_emulation(cuda, oracle, inputs_mod, dt):
+    """The multi-GPU Reduce-Scan-Scan path on one GPU: the array is split into
+    G contiguous shards; per shard scan_total, an emulated all-gather
+    (torch.cat), carry_from_totals and a scan with carry-in (the same
+    dist.rss_scan host logic the NCCL path runs).  The concatenation must equal
+    the oracle over the whole array (bit-exact for integers)."""
+    from paper_2505_15112_b200.dist import rss_scan, shard_bounds
+    n, G = 3 * (1 << 20) + 12345, 4
+    x = host_input(inputs_mod, dt, n, seed=77)
+    xd = to_dev(x, dt)
+    exclusive = dt == "i8"
+    shards = [xd[slice(*shard_bounds(n, G, r))] for r in range(G)]
+    totals_all = torch.cat([cuda.total(s) for s in shards])
+    outs = []
+    for r, s in enumerate(shards):
+        y, totals, carry = rss_scan(
+            s, exclusive, r, G,
+            local_total=cuda.total,
+            all_gather=lambda t: totals_all,
+            carry_of=lambda totals, rr: cuda.carry_from_totals(totals, rr, s.dtype),
+            local_scan=lambda xl, exc, c: (cuda.exclusive if exc else cuda.inclusive)(xl, carry_in=c))
+        outs.append(y)
+    got = torch.cat(outs)
+    torch.cuda.synchronize()
+    assert_parity(oracle, got, oracle_1d(oracle, x, dt, exclusive), dt)
+    if dt != "f32":
+        whole = (cuda.exclusive if exclusive else cuda.inclusive)(xd)
+        assert torch.equal(got, whole)
