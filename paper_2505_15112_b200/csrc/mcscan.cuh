@@ -49,7 +49,7 @@
 
 namespace scan {
 
-constexpr int kMcProf = 14;
+constexpr int kMcProf = 18;
 
 // Block reductions live in the workspace after the header: r[c][b] (8 bytes
 // each, chunk-major); barrier counters in their own region (kWsBarOffset).
@@ -63,23 +63,27 @@ struct McGeom {
     int g;              // CTAs (blocks per chunk)
 };
 
-// Job q of a CTA's sequence R0 R1 S0 R2 S1 ... R(C-1) S(C-2) S(C-1):
-// returns the chunk and whether it is a scan (S) job.
-__device__ __forceinline__ void mc_job(int64_t q, int64_t chunks, int64_t& c, bool& is_scan)
+// Job q of a CTA's sequence with reductions running `ahead` chunks ahead of
+// scans: R(0)..R(ahead), then S(0) R(ahead+1) S(1) R(ahead+2) ..., then the
+// remaining S jobs.  Returns the chunk and whether it is a scan (S) job.
+__device__ __forceinline__ void mc_job(int64_t q, int64_t chunks, int ahead, int64_t& c, bool& is_scan)
 {
-    if (q == 0) { c = 0; is_scan = false; return; }
-    const int64_t k = q - 1;             // pairs (R(k/2+1), S(k/2)) ...
-    if (chunks == 1) { c = 0; is_scan = true; return; }
-    if (k < 2 * (chunks - 1)) {
-        c = (k & 1) ? (k >> 1) : (k >> 1) + 1;
-        is_scan = (k & 1) != 0;
+    const int64_t F = chunks < ahead + 1 ? chunks : ahead + 1;  // leading reductions
+    if (q < F) {
+        c = q;
+        is_scan = false;
+        return;
+    }
+    const int64_t qq = q - F;
+    const int64_t P = chunks - F;                                  // (S, R) pairs
+    if (qq < 2 * P) {
+        c = (qq & 1) ? (qq >> 1) + F : (qq >> 1);
+        is_scan = (qq & 1) == 0;
     } else {
-        c = chunks - 1;
+        c = P + (qq - 2 * P);
         is_scan = true;
     }
 }
-
-
 
 struct McParams16 {
     CUtensorMap tm_in;      // 2-D [rows x 128 B] view of the input (unused for int8)
@@ -93,6 +97,7 @@ struct McParams16 {
     int64_t n_tma_out;      // elements covered by tm_out (full rows)
     int exclusive;
     int debug;
+    int ahead;              // reduce jobs run this many chunks ahead of scan jobs (1..2)
 };
 
 template <int DT, int NC, int GPW, int NB_IN, int NB_OUT>
@@ -105,13 +110,20 @@ struct Mc16Cfg {
     static constexpr size_t kOutSlot = (size_t)kTile * 4;
     static constexpr int kRowElemsIn = 128 / (int)sizeof(In);          // elements per 128-B row
     // TMA boxes: up to 256 rows of 128 B each (the box-dimension limit)
-    static constexpr int kBoxRowsIn = kInSlot / 128 < 256 ? (int)(kInSlot / 128) : 256;
-    static constexpr int kBoxRowsOut = kOutSlot / 128 < 256 ? (int)(kOutSlot / 128) : 256;
+    static constexpr int box_rows(size_t rows)
+    {
+        for (int k = 1; k <= 64; ++k)
+            if (rows % k == 0 && rows / k <= 256 && (rows / k) % 8 == 0) return (int)(rows / k);
+        return 0;
+    }
+    static constexpr int kBoxRowsIn = box_rows(kInSlot / 128);
+    static constexpr int kBoxRowsOut = box_rows(kOutSlot / 128);
     static constexpr int kBoxesIn = sizeof(In) == 1 ? 0 : (int)(kInSlot / (kBoxRowsIn * 128));
     static constexpr int kBoxesOut = (int)(kOutSlot / (kBoxRowsOut * 128));
     static_assert(sizeof(In) == 1 || kInSlot % (kBoxRowsIn * 128) == 0, "whole TMA boxes per tile");
     static_assert(kOutSlot % (kBoxRowsOut * 128) == 0, "whole TMA boxes per tile");
-    static_assert(kBoxRowsIn % 8 == 0 && kBoxRowsOut % 8 == 0, "boxes keep the 1024-B swizzle phase");
+    static_assert(sizeof(In) == 1 || kBoxRowsIn > 0, "input boxes of whole 1024-B swizzle phases");
+    static_assert(kBoxRowsOut > 0, "output boxes of whole 1024-B swizzle phases");
     static constexpr size_t kSmem = NB_IN * kInSlot + NB_OUT * kOutSlot + 1024;  // + alignment slack
 };
 
@@ -227,6 +239,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     using Carry = typename Tr::Carry;
     constexpr int TILE = Cfg::kTile;
     constexpr int KC = 4;
+    constexpr int RS = 4;  // reduce-sum hand-off ring (ahead <= 2)
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* const smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -238,10 +251,10 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     __shared__ __align__(8) uint64_t store_ready[NB_OUT];
     __shared__ __align__(8) uint64_t out_empty[NB_OUT];
     __shared__ __align__(8) uint64_t carry_ready[KC];
-    __shared__ __align__(8) uint64_t rsum_ready[2];
+    __shared__ __align__(8) uint64_t rsum_ready[RS];
     __shared__ int64_t s_store_g0[NB_OUT];
     __shared__ Acc s_wt[2][NC];
-    __shared__ Carry s_job_sum[2][NC];
+    __shared__ Carry s_job_sum[RS][NC];
     __shared__ Carry s_carry[KC];
     __shared__ unsigned long long s_prof[kMcProf];
 
@@ -271,7 +284,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
             ptx::mbar_init(&out_empty[o], 1);
         }
         for (int k = 0; k < KC; ++k) ptx::mbar_init(&carry_ready[k], 1);
-        for (int k = 0; k < 2; ++k) ptx::mbar_init(&rsum_ready[k], NC);
+        for (int k = 0; k < RS; ++k) ptx::mbar_init(&rsum_ready[k], NC);
         ptx::fence_mbar_init();
     }
     __syncthreads();
@@ -292,13 +305,13 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
             for (int64_t q = 0; q < njobs; ++q) {
                 int64_t c;
                 bool is_scan;
-                mc_job(q, gm.chunks, c, is_scan);
+                mc_job(q, gm.chunks, p.ahead, c, is_scan);
                 int64_t lo, hi;
                 block_range(c, lo, hi);
                 for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++q_tile) {
                     const int s = (int)(q_tile % NB_IN);
                     const uint32_t use = (uint32_t)(q_tile / NB_IN);
-                    if (use > 0) mbar_wait_prof(&in_empty[s], (use - 1) & 1u, prof, &s_prof[0]);
+                    if (use > 0) ptx::mbar_wait(&in_empty[s], (use - 1) & 1u);
                     uint8_t* dst = in_ring + s * Cfg::kInSlot;
                     const uint64_t pol = is_scan ? pol_drop : pol_keep;
                     if constexpr (sizeof(In) == 1) {
@@ -326,16 +339,24 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         if (lane == 0) {
             const uint64_t pol = ptx::policy_evict_first();
             int64_t o_tile = 0;
+            int pend = -1;  // out slot whose store may still be reading shared memory
             for (int64_t q = 0; q < njobs; ++q) {
                 int64_t c;
                 bool is_scan;
-                mc_job(q, gm.chunks, c, is_scan);
+                mc_job(q, gm.chunks, p.ahead, c, is_scan);
                 if (!is_scan) continue;
                 int64_t lo, hi;
                 block_range(c, lo, hi);
                 for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++o_tile) {
                     const int o = (int)(o_tile % NB_OUT);
-                    mbar_wait_prof(&store_ready[o], (uint32_t)(o_tile / NB_OUT) & 1u, prof, &s_prof[5]);
+                    const uint32_t par = (uint32_t)(o_tile / NB_OUT) & 1u;
+                    if (pend >= 0 && !ptx::mbar_try_wait(&store_ready[o], par)) {
+                        // about to block: release the pending slot first
+                        ptx::bulk_wait_read<0>();
+                        ptx::mbar_arrive(&out_empty[pend]);
+                        pend = -1;
+                    }
+                    mbar_wait_prof(&store_ready[o], par, prof, &s_prof[5]);
                     if (g0 < p.n_tma_out) {
                         const int y0 = (int)(g0 / 32);
 #pragma unroll
@@ -343,11 +364,16 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                             tma_store_2d(&p.tm_out, 0, y0 + Cfg::kBoxRowsOut * k,
                                          out_ring + o * Cfg::kOutSlot + k * Cfg::kBoxRowsOut * 128, pol);
                         ptx::bulk_commit();
-                        const long long w0 = prof ? clock64() : 0;
-                        ptx::bulk_wait_read<0>();
-                        if (prof) atomicAdd(&s_prof[6], (unsigned long long)(clock64() - w0));
+                        if (pend >= 0) {  // keep two stores in flight; retire the older one
+                            const long long w0 = prof ? clock64() : 0;
+                            ptx::bulk_wait_read<1>();
+                            if (prof) atomicAdd(&s_prof[6], (unsigned long long)(clock64() - w0));
+                            ptx::mbar_arrive(&out_empty[pend]);
+                        }
+                        pend = o;
+                    } else {
+                        ptx::mbar_arrive(&out_empty[o]);
                     }
-                    ptx::mbar_arrive(&out_empty[o]);
                 }
             }
             ptx::bulk_wait<0>();
@@ -362,51 +388,69 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 chunk_carry = (uint32_t)(uint64_t)(*reinterpret_cast<const int64_t*>(p.carry_in));
         }
         constexpr int RPL = kMaxGridPerLane;
-        auto publish = [&](int64_t c) {
-            ptx::mbar_wait(&rsum_ready[c & 1], (uint32_t)(c >> 1) & 1u);
-            if (lane == 0) {
-                Carry t = Carry(0);
-                for (int w = 0; w < NC; ++w) t = t + s_job_sum[c & 1][w];
-                r_all[c * gm.g + b] = carry_bits(t);
-                __threadfence();
-                atomicAdd(&bar[c], 1u);
-            }
-            __syncwarp();
-        };
-        publish(0);
-        for (int64_t c = 0; c < gm.chunks; ++c) {
-            if (c + 1 < gm.chunks) publish(c + 1);
-            if (lane == 0) {
-                const long long w0 = prof ? clock64() : 0;
-                uint32_t backoff = 32;
-                while (ld_acquire_u32(&bar[c]) < (uint32_t)gm.g) {
-                    __nanosleep(backoff);
-                    backoff = backoff < 256 ? backoff * 2 : 256;
+        // Event loop: publish r[c][b] as soon as the compute warps' reduction
+        // of chunk c is in (fixed-order sum of their sums, release-add on the
+        // chunk barrier), and form the carry of chunk c as soon as its barrier
+        // is complete (SyncAll P245; partial = sum of the first b entries of r,
+        // P248) -- whichever is ready first, so neither waits on the other.
+        int64_t next_pub = 0, next_car = 0;
+        uint32_t backoff = 32;
+        long long spin0 = 0;
+        while (next_car < gm.chunks) {
+            bool progressed = false;
+            if (next_pub < gm.chunks &&
+                ptx::mbar_try_wait(&rsum_ready[next_pub % RS], (uint32_t)(next_pub / RS) & 1u)) {
+                if (lane == 0) {
+                    Carry t = Carry(0);
+                    for (int w = 0; w < NC; ++w) t = t + s_job_sum[next_pub % RS][w];
+                    r_all[next_pub * gm.g + b] = carry_bits(t);
+                    ptx::red_release_add_u32(&bar[next_pub], 1u);  // orders the r store before the arrival
                 }
-                if (prof) s_prof[4] += (unsigned long long)(clock64() - w0);
+                __syncwarp();
+                ++next_pub;
+                progressed = true;
             }
-            __syncwarp();
-            uint64_t rb[RPL];
+            if (next_car < next_pub) {
+                uint32_t arrived = lane == 0 ? ld_acquire_u32(&bar[next_car]) : 0u;
+                arrived = __shfl_sync(0xffffffffu, arrived, 0);
+                if (arrived >= (uint32_t)gm.g) {
+                    const int64_t c = next_car;
+                    uint64_t rb[RPL];
 #pragma unroll
-            for (int k = 0; k < RPL; ++k) {
-                const int bb = lane + 32 * k;
-                rb[k] = bb < gm.g ? ld_relaxed_u64(&r_all[c * gm.g + bb]) : 0ull;
-            }
-            Carry below = Carry(0), total = Carry(0);
+                    for (int k = 0; k < RPL; ++k) {
+                        const int bb = lane + 32 * k;
+                        rb[k] = bb < gm.g ? ld_relaxed_u64(&r_all[c * gm.g + bb]) : 0ull;
+                    }
+                    Carry below = Carry(0), total = Carry(0);
 #pragma unroll
-            for (int k = 0; k < RPL; ++k) {
-                const int bb = lane + 32 * k;
-                const Carry v = bb < gm.g ? carry_from_bits<Carry>(rb[k]) : Carry(0);
-                total = total + v;
-                if (bb < b) below = below + v;
+                    for (int k = 0; k < RPL; ++k) {
+                        const int bb = lane + 32 * k;
+                        const Carry v = bb < gm.g ? carry_from_bits<Carry>(rb[k]) : Carry(0);
+                        total = total + v;
+                        if (bb < b) below = below + v;
+                    }
+                    below = warp_reduce_fixed(below);
+                    total = warp_reduce_fixed(total);
+                    if (lane == 0) {
+                        s_carry[c % KC] = chunk_carry + below;
+                        ptx::mbar_arrive(&carry_ready[c % KC]);
+                    }
+                    chunk_carry = chunk_carry + total;
+                    ++next_car;
+                    progressed = true;
+                }
             }
-            below = warp_reduce_fixed(below);
-            total = warp_reduce_fixed(total);
-            if (lane == 0) {
-                s_carry[c % KC] = chunk_carry + below;
-                ptx::mbar_arrive(&carry_ready[c % KC]);
+            if (progressed) {
+                backoff = 32;
+                if (prof && lane == 0 && spin0) {
+                    s_prof[4] += (unsigned long long)(clock64() - spin0);
+                    spin0 = 0;
+                }
+            } else {
+                if (prof && lane == 0 && !spin0) spin0 = clock64();
+                __nanosleep(backoff);
+                backoff = backoff < 256 ? backoff * 2 : 256;
             }
-            chunk_carry = chunk_carry + total;
         }
     } else {
         // =========================== compute ===========================
@@ -434,7 +478,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         for (int64_t q = 0; q < njobs; ++q) {
             int64_t c;
             bool is_scan;
-            mc_job(q, gm.chunks, c, is_scan);
+            mc_job(q, gm.chunks, p.ahead, c, is_scan);
             int64_t lo, hi;
             block_range(c, lo, hi);
             if (!is_scan) {
@@ -471,13 +515,13 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 }
                 jsum = warp_reduce_fixed(jsum);
                 if (lane == 0) {
-                    s_job_sum[c & 1][cw] = jsum;
-                    ptx::mbar_arrive(&rsum_ready[c & 1]);
+                    s_job_sum[c % RS][cw] = jsum;
+                    ptx::mbar_arrive(&rsum_ready[c % RS]);
                 }
             } else {
                 // ---------------- Phase II: scan with the block carry ----------------
                 mbar_wait_prof(&carry_ready[c % KC], (uint32_t)(c / KC) & 1u, prof && cw == 0 && lane == 0,
-                               &s_prof[4]);
+                               &s_prof[0]);
                 Carry carry = s_carry[c % KC];
                 for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++q_tile, ++o_tile, ++s_count) {
                     const int s = (int)(q_tile % NB_IN);
@@ -519,11 +563,12 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     const Acc xe = __shfl_up_sync(0xffffffffu, xi, 1);
                     const Acc wpref = __shfl_sync(0xffffffffu, lane == 0 ? Acc(0) : xe, cw);
                     const Acc agg = __shfl_sync(0xffffffffu, xi, NC - 1);
-
+                    const long long te0 = clock64();
                     if (o_tile >= NB_OUT)
                         mbar_wait_prof(&out_empty[o], (uint32_t)(o_tile / NB_OUT - 1) & 1u,
                                        prof && cw == 0 && lane == 0, &s_prof[3]);
                     uint8_t* ost = out_ring + o * Cfg::kOutSlot;
+                    const long long te1 = clock64();
 #pragma unroll
                     for (int g = 0; g < GPW; ++g) {
                         const int e0 = (cw * GPW + g) * 512 + 16 * lane;
@@ -554,8 +599,16 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                             }
                         }
                     }
+                    const long long te2 = clock64();
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
+                    const long long te3 = clock64();
+                    if (prof && cw == 0 && lane == 0) {
+                        s_prof[14] += (unsigned long long)(te0 - ts2);
+                        s_prof[15] += (unsigned long long)(te1 - te0);
+                        s_prof[16] += (unsigned long long)(te2 - te1);
+                        s_prof[17] += (unsigned long long)(te3 - te2);
+                    }
                     if (lane == 0) {
                         if (cw == 0) s_store_g0[o] = g0;
                         ptx::mbar_arrive(&store_ready[o]);

@@ -222,6 +222,7 @@ struct Mc16Variant {
         p.ws = sp.ws;
         p.exclusive = sp.exclusive;
         p.debug = debug_bits();
+        p.ahead = env_int("SCAN_MC_AHEAD", 1);
         p.gm.n = n;
         p.gm.tile = kTile;
         p.gm.g = di.sms < kMaxGrid ? di.sms : kMaxGrid;
@@ -275,11 +276,14 @@ int launch_mc(const ScanParams& p, cudaStream_t s, const DevInfo& di)
         else if constexpr (DT == SCAN_F16_F32) return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 2>, DT>(p, s, di);
         else return launch_mc_sized<Mc16Variant<DT, 16, 2, 4, 2>, DT>(p, s, di);
     case 4:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 1, 4, 2>, DT>(p, s, di);
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 1, 3, 3>, DT>(p, s, di);
         else return launch_mc_sized<Mc16Variant<DT, 16, 1, 4, 3>, DT>(p, s, di);
     case 5:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 8, 4, 2, 1>, DT>(p, s, di);
-        else return launch_mc_sized<Mc16Variant<DT, 8, 4, 3, 2>, DT>(p, s, di);
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 12, 2, 2, 2>, DT>(p, s, di);
+        else return launch_mc_sized<Mc16Variant<DT, 12, 2, 3, 2>, DT>(p, s, di);
+    case 6:
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 24, 1, 2, 2>, DT>(p, s, di);
+        else return launch_mc_sized<Mc16Variant<DT, 24, 1, 3, 2>, DT>(p, s, di);
     default:
         if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 2, 2, 1>, DT>(p, s, di);
         else if constexpr (DT == SCAN_F16_F32) return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 2>, DT>(p, s, di);
