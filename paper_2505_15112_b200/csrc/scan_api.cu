@@ -14,6 +14,7 @@
 #include "scan_kernels.cuh"
 #include "scan_ws.cuh"
 #include "mcscan.cuh"
+#include "rowscan.cuh"
 
 using namespace scan;
 
@@ -291,6 +292,79 @@ int launch_mc(const ScanParams& p, cudaStream_t s, const DevInfo& di)
     }
 }
 
+// ---- batched rows of many tiles: one CTA per row (rowscan.cuh) -------------------
+bool encode_rows3d(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int64_t stride_elems,
+                   int elem_bytes, int box_rows)
+{
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)(128 / elem_bytes), (cuuint64_t)(cols * elem_bytes / 128),
+                                (cuuint64_t)rows};
+    const cuuint64_t strides[2] = {128, (cuuint64_t)(stride_elems * elem_bytes)};
+    const cuuint32_t box[3] = {(cuuint32_t)(128 / elem_bytes), (cuuint32_t)box_rows, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    const CUtensorMapDataType dt = elem_bytes == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+    return fn(tm, dt, 3, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int DT, int NC, int GPW, int NB>
+struct RowVariant {
+    using Cfg = RowCfg<DT, NC, GPW, NB>;
+    static int launch(const ScanParams& sp, cudaStream_t s, const DevInfo& di)
+    {
+        using In = typename Traits<DT>::In;
+        static std::once_flag once;
+        static cudaError_t err = cudaSuccess;
+        std::call_once(once, [] {
+            err = cudaFuncSetAttribute(k_rowscan16<DT, NC, GPW, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)Cfg::kSmem);
+        });
+        if (err != cudaSuccess) return SCAN_ERR_CUDA;
+        RowParams p;
+        memset(&p, 0, sizeof(p));
+        if constexpr (sizeof(In) != 1) {
+            if (!encode_rows3d(&p.tm_in, sp.in, sp.num_segs, sp.seg_len, sp.in_stride, (int)sizeof(In),
+                               Cfg::kBoxRowsIn))
+                return SCAN_ERR_CUDA;
+        }
+        if (!encode_rows3d(&p.tm_out, sp.out, sp.num_segs, sp.seg_len, sp.out_stride, 4, Cfg::kBoxRowsOut))
+            return SCAN_ERR_CUDA;
+        p.in = sp.in;
+        p.out = sp.out;
+        p.ws = sp.ws;
+        p.rows = sp.num_segs;
+        p.cols = sp.seg_len;
+        p.in_stride = sp.in_stride;
+        p.tiles_per_row = (int)((sp.seg_len + Cfg::kTile - 1) / Cfg::kTile);
+        p.exclusive = sp.exclusive;
+        int64_t grid = di.sms;
+        if (grid > sp.num_segs) grid = sp.num_segs;
+        k_rowscan16<DT, NC, GPW, NB><<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(p);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+    }
+};
+
+template <int DT>
+bool rowscan_ok(const ScanParams& p)
+{
+    using In = typename Traits<DT>::In;
+    return p.num_segs > 1 && p.tma_in && p.tma_out && (p.seg_len * (int64_t)sizeof(In)) % 128 == 0 &&
+           (p.seg_len * 4) % 128 == 0 && p.num_segs < (1ll << 31) && env_int("SCAN_NO_ROWSCAN", 0) == 0;
+}
+
+template <int DT>
+int launch_rows(const ScanParams& p, cudaStream_t s, const DevInfo& di)
+{
+    switch (env_int("SCAN_ROWS", 0)) {
+    case 1: return RowVariant<DT, 16, 1, 6>::launch(p, s, di);
+    case 2: return RowVariant<DT, 16, 2, 2>::launch(p, s, di);
+    default: return RowVariant<DT, 16, 2, 3>::launch(p, s, di);
+    }
+}
+
 // Single-tile-per-segment (static) and tuning-alternative kernels; the default
 // path for multi-tile segments is the warp-specialized kernel.  SCAN_VARIANT
 // selects alternatives for experiments.
@@ -305,6 +379,7 @@ int launch_dt(ScanParams p, cudaStream_t s, const DevInfo& di)
         if (p.num_segs == 1 && p.tma_in && p.tma_out && p.seg_len >= kMcMinElems &&
             env_int("SCAN_NO_MC", 0) == 0)
             return launch_mc<DT>(p, s, di);
+        if (rowscan_ok<DT>(p)) return launch_rows<DT>(p, s, di);
         if constexpr (wide_in) {
             return WsVariant<DT, 16, 3, 8, 3, 3>::launch(p, s, di);
         } else if constexpr (DT == SCAN_F16_F32) {

@@ -281,3 +281,22 @@ def test_sharded_emulation(cuda, oracle, inputs_mod, dt):
     if dt != "f32":
         whole = (cuda.exclusive if exclusive else cuda.inclusive)(xd)
         assert torch.equal(got, whole)
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+def test_rows_many_tiles_strided(cuda, oracle, inputs_mod, dt):
+    """Rows of several tiles with a ragged last tile and padded (16-byte
+    aligned) row strides: the one-CTA-per-row kernel (rowscan.cuh)."""
+    R = 13
+    C = 40064 if dt == "i8" else 40000
+    S = C + 128
+    x = host_input(inputs_mod, dt, R * S, seed=4242).reshape(R, S)
+    xd = to_dev(x, dt)[:, :C]
+    out_b = torch.empty((R, C + 64), dtype=torch.int32 if dt in ("i32", "i8") else torch.float32,
+                        device="cuda")
+    for exc in (False, True):
+        out = out_b[:, :C]
+        cuda.rows(xd, exclusive=exc, out=out)
+        torch.cuda.synchronize()
+        for r in range(R):
+            assert_parity(oracle, out[r], oracle_1d(oracle, np.ascontiguousarray(x[r, :C]), dt, exc), dt)
