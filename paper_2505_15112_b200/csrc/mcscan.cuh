@@ -124,7 +124,12 @@ struct Mc16Cfg {
     static_assert(kOutSlot % (kBoxRowsOut * 128) == 0, "whole TMA boxes per tile");
     static_assert(sizeof(In) == 1 || kBoxRowsIn > 0, "input boxes of whole 1024-B swizzle phases");
     static_assert(kBoxRowsOut > 0, "output boxes of whole 1024-B swizzle phases");
-    static constexpr size_t kSmem = NB_IN * kInSlot + NB_OUT * kOutSlot + 1024;  // + alignment slack
+    // NB_OUT == 0: unified ring -- NB_IN slots of kOutSlot bytes; a scan tile's
+    // outputs are written in place over its input after the per-tile named
+    // barrier, and the storer frees the slot once its store has read it.
+    static constexpr bool kUni = NB_OUT == 0;
+    static constexpr size_t kRingSlot = kUni ? kOutSlot : kInSlot;
+    static constexpr size_t kSmem = kUni ? NB_IN * kOutSlot + 1024 : NB_IN * kInSlot + NB_OUT * kOutSlot + 1024;
 };
 
 // ---- 16 contiguous elements of lane-offset e0 from a swizzled slot -----------
@@ -243,16 +248,18 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* const smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    constexpr bool UNI = Cfg::kUni;
+    constexpr int NSR = UNI ? NB_IN : NB_OUT;  // store_ready / out slots
     uint8_t* const in_ring = smem;
-    uint8_t* const out_ring = smem + NB_IN * Cfg::kInSlot;
+    uint8_t* const out_ring = UNI ? smem : smem + NB_IN * Cfg::kInSlot;
 
     __shared__ __align__(8) uint64_t in_full[NB_IN];
     __shared__ __align__(8) uint64_t in_empty[NB_IN];
-    __shared__ __align__(8) uint64_t store_ready[NB_OUT];
-    __shared__ __align__(8) uint64_t out_empty[NB_OUT];
+    __shared__ __align__(8) uint64_t store_ready[NSR];
+    __shared__ __align__(8) uint64_t out_empty[NSR];
     __shared__ __align__(8) uint64_t carry_ready[KC];
     __shared__ __align__(8) uint64_t rsum_ready[RS];
-    __shared__ int64_t s_store_g0[NB_OUT];
+    __shared__ int64_t s_store_g0[NSR];
     __shared__ Acc s_wt[2][NC];
     __shared__ Carry s_job_sum[RS][NC];
     __shared__ Carry s_carry[KC];
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
             ptx::mbar_init(&in_full[s], 1);
             ptx::mbar_init(&in_empty[s], NC);
         }
-        for (int o = 0; o < NB_OUT; ++o) {
+        for (int o = 0; o < NSR; ++o) {
             ptx::mbar_init(&store_ready[o], NC);
             ptx::mbar_init(&out_empty[o], 1);
         }
@@ -312,7 +319,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     const int s = (int)(q_tile % NB_IN);
                     const uint32_t use = (uint32_t)(q_tile / NB_IN);
                     if (use > 0) ptx::mbar_wait(&in_empty[s], (use - 1) & 1u);
-                    uint8_t* dst = in_ring + s * Cfg::kInSlot;
+                    uint8_t* dst = in_ring + s * Cfg::kRingSlot;
                     const uint64_t pol = is_scan ? pol_drop : pol_keep;
                     if constexpr (sizeof(In) == 1) {
                         int64_t m_tma = p.n_tma_in - g0;
@@ -338,25 +345,36 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         // =========================== storer ===========================
         if (lane == 0) {
             const uint64_t pol = ptx::policy_evict_first();
-            int64_t o_tile = 0;
-            int pend = -1;  // out slot whose store may still be reading shared memory
+            int64_t o_tile = 0, q_tile = 0;
+            uint32_t sparity = 0;  // UNI: bit s = parity of the next store_ready[s] phase
+            int pend = -1;         // slot whose store may still be reading shared memory
+            auto release = [&](int slot) {
+                if (UNI)
+                    ptx::mbar_arrive_cnt(&in_empty[slot], NC);  // counts as the NC compute arrivals
+                else
+                    ptx::mbar_arrive(&out_empty[slot]);
+            };
             for (int64_t q = 0; q < njobs; ++q) {
                 int64_t c;
                 bool is_scan;
                 mc_job(q, gm.chunks, p.ahead, c, is_scan);
-                if (!is_scan) continue;
                 int64_t lo, hi;
                 block_range(c, lo, hi);
-                for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++o_tile) {
-                    const int o = (int)(o_tile % NB_OUT);
-                    const uint32_t par = (uint32_t)(o_tile / NB_OUT) & 1u;
+                if (!is_scan) {
+                    if (UNI) q_tile += (hi - lo + TILE - 1) / TILE;
+                    continue;
+                }
+                for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++o_tile, ++q_tile) {
+                    const int o = UNI ? (int)(q_tile % NB_IN) : (int)(o_tile % NB_OUT);
+                    const uint32_t par = UNI ? ((sparity >> o) & 1u) : (uint32_t)(o_tile / NB_OUT) & 1u;
                     if (pend >= 0 && !ptx::mbar_try_wait(&store_ready[o], par)) {
                         // about to block: release the pending slot first
                         ptx::bulk_wait_read<0>();
-                        ptx::mbar_arrive(&out_empty[pend]);
+                        release(pend);
                         pend = -1;
                     }
                     mbar_wait_prof(&store_ready[o], par, prof, &s_prof[5]);
+                    if (UNI) sparity ^= 1u << o;
                     if (g0 < p.n_tma_out) {
                         const int y0 = (int)(g0 / 32);
 #pragma unroll
@@ -368,11 +386,11 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                             const long long w0 = prof ? clock64() : 0;
                             ptx::bulk_wait_read<1>();
                             if (prof) atomicAdd(&s_prof[6], (unsigned long long)(clock64() - w0));
-                            ptx::mbar_arrive(&out_empty[pend]);
+                            release(pend);
                         }
                         pend = o;
                     } else {
-                        ptx::mbar_arrive(&out_empty[o]);
+                        release(o);
                     }
                 }
             }
@@ -492,7 +510,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     const int m = (int)(hi - g0 < TILE ? hi - g0 : TILE);
                     int64_t mt = p.n_tma_in - g0;
                     const int m_tma = (int)(mt < 0 ? 0 : (mt > m ? m : mt));
-                    const uint8_t* slot = in_ring + s * Cfg::kInSlot;
+                    const uint8_t* slot = in_ring + s * Cfg::kRingSlot;
 #pragma unroll
                     for (int g = 0; g < GPW; ++g) {
                         const int e0 = (cw * GPW + g) * 512 + 16 * lane;
@@ -525,14 +543,14 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 Carry carry = s_carry[c % KC];
                 for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++q_tile, ++o_tile, ++s_count) {
                     const int s = (int)(q_tile % NB_IN);
-                    const int o = (int)(o_tile % NB_OUT);
+                    const int o = UNI ? s : (int)(o_tile % NB_OUT);
                     mbar_wait_prof(&in_full[s], (uint32_t)(q_tile / NB_IN) & 1u, prof && cw == 0 && lane == 0,
                                    &s_prof[2]);
                     const long long ts0 = clock64();
                     const int m = (int)(hi - g0 < TILE ? hi - g0 : TILE);
                     int64_t mt = p.n_tma_in - g0;
                     const int m_tma = (int)(mt < 0 ? 0 : (mt > m ? m : mt));
-                    const uint8_t* slot = in_ring + s * Cfg::kInSlot;
+                    const uint8_t* slot = in_ring + s * Cfg::kRingSlot;
 
                     Acc v[GPW][16];
                     Acc ex[GPW], gp[GPW];
@@ -544,8 +562,10 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
 #pragma unroll
                         for (int k = 1; k < 16; ++k) v[g][k] = v[g][k - 1] + v[g][k];
                     }
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&in_empty[s]);
+                    if (!UNI) {  // unified ring: the storer frees the slot after the store
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(&in_empty[s]);
+                    }
 #pragma unroll
                     for (int g = 0; g < GPW; ++g) {
                         const Acc incl = warp_incl_scan(v[g][15], lane);
@@ -564,7 +584,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     const Acc wpref = __shfl_sync(0xffffffffu, lane == 0 ? Acc(0) : xe, cw);
                     const Acc agg = __shfl_sync(0xffffffffu, xi, NC - 1);
                     const long long te0 = clock64();
-                    if (o_tile >= NB_OUT)
+                    if (!UNI && o_tile >= NB_OUT)
                         mbar_wait_prof(&out_empty[o], (uint32_t)(o_tile / NB_OUT - 1) & 1u,
                                        prof && cw == 0 && lane == 0, &s_prof[3]);
                     uint8_t* ost = out_ring + o * Cfg::kOutSlot;

@@ -97,6 +97,40 @@ struct Variant {
         return err == cudaSuccess ? occ : -1;
     }
 
+    // Small 1-D n (2..16 tiles): one cluster, one tile per CTA, DSMEM carries.
+    static int launch_cluster(ScanParams p, cudaStream_t s)
+    {
+        static std::once_flag once;
+        static cudaError_t err = cudaSuccess;
+        auto kern = k_scan_tiles<DT, TH, RW, ST, OS, MB>;
+        std::call_once(once, [&] {
+            err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+            if (err == cudaSuccess)
+                err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        });
+        if (err != cudaSuccess) return SCAN_ERR_CUDA;
+        p.tiles_per_seg = (p.seg_len + kTile - 1) / kTile;
+        p.num_tiles = p.tiles_per_seg;
+        p.static_sched = 1;
+        p.cluster = (int)p.num_tiles;
+        p.debug = 0;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)p.num_tiles);
+        cfg.blockDim = dim3(TH);
+        cfg.dynamicSmemBytes = kSmem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)p.num_tiles;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return e == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+    }
+
     static int launch(ScanParams p, cudaStream_t s, const DevInfo& di)
     {
         int occ = occupancy();
@@ -104,6 +138,7 @@ struct Variant {
         p.tiles_per_seg = (p.seg_len + kTile - 1) / kTile;
         p.num_tiles = p.tiles_per_seg * p.num_segs;
         p.static_sched = p.tiles_per_seg == 1;
+        p.cluster = 0;
         p.debug = debug_bits();
         int64_t grid = (int64_t)di.sms * occ;
         if (grid > p.num_tiles) grid = p.num_tiles;
@@ -285,6 +320,13 @@ int launch_mc(const ScanParams& p, cudaStream_t s, const DevInfo& di)
     case 6:
         if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 24, 1, 2, 2>, DT>(p, s, di);
         else return launch_mc_sized<Mc16Variant<DT, 24, 1, 3, 2>, DT>(p, s, di);
+    case 7: return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 0>, DT>(p, s, di);   // unified in-place ring
+    case 8:
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 12, 2, 3, 1>, DT>(p, s, di);
+        else return launch_mc_sized<Mc16Variant<DT, 16, 2, 6, 2>, DT>(p, s, di);
+    case 9:
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 24, 1, 3, 1>, DT>(p, s, di);
+        else return launch_mc_sized<Mc16Variant<DT, 12, 2, 4, 2>, DT>(p, s, di);
     default:
         if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 2, 2, 1>, DT>(p, s, di);
         else if constexpr (DT == SCAN_F16_F32) return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 2>, DT>(p, s, di);
@@ -376,6 +418,8 @@ int launch_dt(ScanParams p, cudaStream_t s, const DevInfo& di)
     const int v = variant();
     if (v == 0 || p.seg_len <= Small::kTile) {
         if (p.seg_len <= Small::kTile) return Small::launch(p, s, di);
+        if (p.num_segs == 1 && p.seg_len <= 16 * (int64_t)Small::kTile && env_int("SCAN_NO_CLUSTER", 0) == 0)
+            return Small::launch_cluster(p, s);
         if (p.num_segs == 1 && p.tma_in && p.tma_out && p.seg_len >= kMcMinElems &&
             env_int("SCAN_NO_MC", 0) == 0)
             return launch_mc<DT>(p, s, di);

@@ -184,6 +184,27 @@ __device__ __forceinline__ uint32_t carry_from_bits<uint32_t>(uint64_t b) { retu
 template <>
 __device__ __forceinline__ double carry_from_bits<double>(uint64_t b) { return __longlong_as_double((long long)b); }
 
+// ---- thread-block cluster helpers (small-n path) ----
+__device__ __forceinline__ uint32_t cluster_ctarank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Read a 64-bit word from the shared memory of CTA `rank` of this cluster.
+__device__ __forceinline__ uint64_t ld_dsmem_u64(const void* local_smem_ptr, uint32_t rank)
+{
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(ptx::smem_u32(local_smem_ptr)), "r"(rank));
+    uint64_t v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(remote) : "memory");
+    return v;
+}
+
 using ptx::ld_acquire_u32;
 using ptx::ld_acquire_u64;
 using ptx::ld_relaxed_u64;
@@ -366,6 +387,7 @@ struct ScanParams {
     int tma_in;             // segment bases and strides 16-byte aligned (input)
     int tma_out;            // same for output
     int static_sched;       // one tile per segment: no tickets, no look-back
+    int cluster;            // > 0: small-n mode, one tile per CTA of ONE cluster, carries via DSMEM
     int debug;              // bit 0: skip look-back (timing only; wrong results); bit 1: spin without
                             // nanosleep; bit 2: per-CTA stall counters into the workspace
 };
@@ -411,6 +433,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
     __shared__ Acc s_warp_pref[NW];
     __shared__ Carry s_prefix;
     __shared__ uint32_t s_epoch;
+    __shared__ uint64_t s_cl_agg;  // cluster mode: this CTA's tile aggregate (Carry bits)
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -550,7 +573,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
                     carry_seg = (uint32_t)(uint64_t)(*reinterpret_cast<const int64_t*>(p.carry_in));
             }
             Carry prefix;
-            if (k == 0) {
+            if (p.cluster) {
+                prefix = carry_seg;  // + lower CTAs' aggregates, added after the cluster barrier
+                if (lane == 0) s_cl_agg = carry_bits(Carry(agg));
+            } else if (k == 0) {
                 prefix = carry_seg;
                 if (!p.static_sched && p.tiles_per_seg > 1 && lane == 0)
                     Desc<Carry>::publish(desc + t * Desc<Carry>::kSlots, true, tag,
@@ -573,6 +599,21 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
             last_t = t;
             last_incl = prefix + Carry(agg);
             if (lane == 0) s_prefix = prefix;
+        }
+        if (p.cluster) {
+            // Small n: the tiles are the CTAs of one cluster.  Every CTA posts
+            // its aggregate in its own shared memory; after a cluster barrier
+            // warp 0 sums the aggregates of the lower-ranked CTAs over DSMEM
+            // (fixed lane-tree order) -- no global descriptors, no atomics.
+            cluster_sync_all();
+            if (warp == 0) {
+                const uint32_t rank = cluster_ctarank();
+                Carry v = Carry(0);
+                if ((uint32_t)lane < rank) v = carry_from_bits<Carry>(ld_dsmem_u64(&s_cl_agg, (uint32_t)lane));
+                v = warp_reduce_fixed(v);
+                if (lane == 0) s_prefix = s_prefix + v;
+            }
+            cluster_sync_all();  // no CTA leaves while another may still read its shared memory
         }
         // The output staging buffer we are about to fill must no longer be
         // read by the bulk store issued OSTAGES tiles ago.
