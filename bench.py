@@ -386,16 +386,25 @@ def run_ours(args, rank, world, local_rank):
 
 
 def run_e2e(args, x, out, out2, scan_call, dev, stream, world, barrier, local_elems, w, step_bytes):
-    """Same metric through the public API with HOST buffers: every step copies
-    the input from pinned host memory, scans, and copies the result back."""
+    """Same metric through the public API with HOST buffers: every step moves
+    the input from pinned host memory and the result back.  1-D scans use the
+    library's pipelined host path (scan_host: chunked H2D / scan / D2H on
+    three streams); rows and C1 copy whole arrays around the device call."""
     import torch
+
+    import paper_2505_15112_b200 as S
     h_in = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
     h_in.copy_(x)
     h_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
     h_out2 = torch.empty(out.shape, dtype=out.dtype, pin_memory=True) if out2 is not None else None
     steps = max(1, min(args.steps, args.e2e_steps))
+    pipelined = args.config in ("C2", "C3", "C5") and world == 1
+    exclusive = "exclusive" in w["ops"]
 
     def step():
+        if pipelined:
+            S.host_scan(h_in, h_out, exclusive=exclusive, chunk=args.e2e_chunk)
+            return
         x.copy_(h_in, non_blocking=True)
         scan_call(x, out, out2)
         h_out.copy_(out, non_blocking=True)
@@ -421,9 +430,10 @@ def run_e2e(args, x, out, out2, scan_call, dev, stream, world, barrier, local_el
         ms = t.item()
     h2d = x.numel() * x.element_size()
     d2h = out.numel() * out.element_size() * (2 if out2 is not None else 1)
+    path = ("pinned host -> scan_host (C ABI: chunked H2D | scan | D2H on 3 streams) -> pinned host"
+            if pipelined else "pinned host -> cudaMemcpyAsync -> scan (C ABI) -> cudaMemcpyAsync -> pinned host")
     return {"value": round(step_bytes / (ms / steps * 1e-3) / 1e9, 2), "unit": "GB/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps,
-            "path": "pinned host -> cudaMemcpyAsync -> scan (C ABI) -> cudaMemcpyAsync -> pinned host"}
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps, "path": path}
 
 
 def main():
@@ -435,6 +445,7 @@ def main():
     ap.add_argument("--config", choices=sorted(WORK), default="C5")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-chunk", type=int, default=1 << 26, help="elements per host-streaming chunk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,

@@ -138,6 +138,22 @@ SCAN_API int scan_total(const void* in, int64_t n, int dtype, void* total_out, v
 SCAN_API int scan_carry_from_totals(const void* totals, int G, int rank, int dtype, void* carry_out,
                            void* stream);
 
+/* End-to-end scan of an array in HOST memory (pinned for full speed): the
+ * array is streamed through the GPU in chunks of `chunk_elems` elements with
+ * the host->device copy of chunk i+1, the scan of chunk i and the
+ * device->host copy of chunk i-1 overlapped on three streams; the carry of
+ * chunk i+1 is the fp64 / int64 running total, kept on the device.  h_in and
+ * h_out are host pointers (h_in != h_out); `stage` is a device buffer of
+ * scan_host_stage_bytes(dtype, chunk_elems) bytes and `ws` a workspace of
+ * scan_workspace_bytes(dtype, chunk_elems) bytes.  Asynchronous with respect
+ * to the host: the result is complete when `stream` reaches the point the
+ * call enqueued (e.g. after cudaStreamSynchronize(stream)).  Semantics are
+ * those of scan_inclusive / scan_exclusive over the whole array, carry 0. */
+SCAN_API size_t scan_host_stage_bytes(int dtype, int64_t chunk_elems);
+SCAN_API int scan_host(const void* h_in, void* h_out, int64_t n, int dtype, int exclusive,
+                       int64_t chunk_elems, void* stage, size_t stage_bytes, void* ws,
+                       size_t ws_bytes, void* stream);
+
 /* Kernel launches the library enqueued since load (a process-wide counter;
  * used by the bench to report how many of its own kernels ran). */
 SCAN_API uint64_t scan_launch_count(void);

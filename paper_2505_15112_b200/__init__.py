@@ -77,6 +77,10 @@ def load() -> ctypes.CDLL:
         L.scan_carry_from_totals.argtypes = [P, I, I, I, P, P]
         L.scan_carry_from_totals.restype = I
         L.scan_launch_count.restype = ctypes.c_uint64
+        L.scan_host_stage_bytes.argtypes = [I, I64]
+        L.scan_host_stage_bytes.restype = SZ
+        L.scan_host.argtypes = [P, P, I64, I, I, I64, P, SZ, P, SZ, P]
+        L.scan_host.restype = I
         _lib = L
     return _lib
 
@@ -210,6 +214,40 @@ def carry_from_totals(totals: torch.Tensor, rank: int, in_dtype: torch.dtype, ou
     _check(load().scan_carry_from_totals(_ptr(totals), totals.numel(), rank, dt, _ptr(out),
                                          _stream_ptr(stream)), "scan_carry_from_totals")
     return out
+
+
+_stage_cache: dict = {}
+
+
+def host_scan(h_in: torch.Tensor, h_out=None, exclusive: bool = False, chunk: int = 1 << 26,
+              device=None, stream=None) -> torch.Tensor:
+    """End-to-end scan of a HOST tensor (pin it for full speed): streamed
+    through the GPU in chunks with H2D copy, scan and D2H copy overlapped
+    (C ABI scan_host).  Returns the host output tensor once complete."""
+    if h_in.is_cuda:
+        raise ScanError("host_scan expects a CPU tensor; use inclusive()/exclusive() for device data")
+    dt, odt, _ = DTYPES[h_in.dtype] if h_in.dtype in DTYPES else (None, None, None)
+    if dt is None:
+        raise ScanError(f"unsupported input dtype {h_in.dtype}")
+    h_in = h_in.reshape(-1)
+    n = h_in.numel()
+    if h_out is None:
+        h_out = torch.empty(n, dtype=odt, pin_memory=h_in.is_pinned())
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    chunk = max(1, min(int(chunk), max(n, 1)))
+    L = load()
+    sb = L.scan_host_stage_bytes(dt, chunk)
+    key = (dev.index, sb)
+    stage = _stage_cache.get(key)
+    if stage is None:
+        stage = torch.empty(sb, dtype=torch.uint8, device=dev)
+        _stage_cache.clear()
+        _stage_cache[key] = stage
+    ws = workspace(L.scan_workspace_bytes(dt, chunk), dev, stream)
+    _check(L.scan_host(ctypes.c_void_p(h_in.data_ptr()), ctypes.c_void_p(h_out.data_ptr()), n, dt,
+                       int(bool(exclusive)), chunk, _ptr(stage), sb, ctypes.c_void_p(ws.ptr), ws.nbytes,
+                       _stream_ptr(stream)), "scan_host")
+    return h_out
 
 
 def launch_count() -> int:

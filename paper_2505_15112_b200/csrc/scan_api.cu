@@ -666,4 +666,94 @@ int scan_carry_from_totals(const void* totals, int G, int rank, int dtype, void*
 
 uint64_t scan_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+// ---- host streaming (end-to-end) ----------------------------------------------------
+// Stage layout: in[2] (chunk x in_size), out[2] (chunk x 4), then a ring of 3
+// carry triples {carry_i, total_i, unused} (8 bytes each, 256-aligned).
+size_t scan_host_stage_bytes(int dtype, int64_t chunk_elems)
+{
+    if (!valid_dt(dtype) || chunk_elems <= 0) return 0;
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    return 2 * up((size_t)chunk_elems * in_size(dtype)) + 2 * up((size_t)chunk_elems * 4) + 256;
+}
+
+int scan_host(const void* h_in, void* h_out, int64_t n, int dtype, int exclusive, int64_t chunk_elems,
+              void* stage, size_t stage_bytes, void* ws, size_t ws_bytes, void* stream)
+{
+    if (!valid_dt(dtype) || n < 0 || chunk_elems <= 0) return SCAN_ERR_ARG;
+    if (n == 0) return SCAN_OK;
+    if (h_in == nullptr || h_out == nullptr || stage == nullptr || h_in == h_out) return SCAN_ERR_ARG;
+    if (stage_bytes < scan_host_stage_bytes(dtype, chunk_elems)) return SCAN_ERR_ARG;
+    DevInfo di;
+    int st = dev_info(di);
+    if (st != SCAN_OK) return st;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    // two copy streams per device, created once (the library's only cached resource besides attributes)
+    static std::mutex mu;
+    static cudaStream_t copy_streams[64][2] = {};
+    {
+        std::lock_guard<std::mutex> g(mu);
+        if (copy_streams[dev][0] == nullptr) {
+            for (int k = 0; k < 2; ++k)
+                if (cudaStreamCreateWithFlags(&copy_streams[dev][k], cudaStreamNonBlocking) != cudaSuccess)
+                    return SCAN_ERR_CUDA;
+        }
+    }
+    cudaStream_t s_c = (cudaStream_t)stream, s_in = copy_streams[dev][0], s_out = copy_streams[dev][1];
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t isz = in_size(dtype), in_b = up((size_t)chunk_elems * isz), out_b = up((size_t)chunk_elems * 4);
+    uint8_t* base = (uint8_t*)stage;
+    uint8_t* d_in[2] = {base, base + in_b};
+    uint8_t* d_out[2] = {base + 2 * in_b, base + 2 * in_b + out_b};
+    uint8_t* trip = base + 2 * in_b + 2 * out_b;  // 3 x {carry, total, unused} x 8 B
+    const int64_t nchunks = (n + chunk_elems - 1) / chunk_elems;
+
+    cudaEvent_t ev_start, ev_in[2], ev_comp[2], ev_out[2];
+    auto mk = [](cudaEvent_t* e) { return cudaEventCreateWithFlags(e, cudaEventDisableTiming) == cudaSuccess; };
+    if (!mk(&ev_start)) return SCAN_ERR_CUDA;
+    for (int k = 0; k < 2; ++k)
+        if (!mk(&ev_in[k]) || !mk(&ev_comp[k]) || !mk(&ev_out[k])) return SCAN_ERR_CUDA;
+    int rc = SCAN_OK;
+    // order after everything already on the caller's stream
+    if (cudaEventRecord(ev_start, s_c) != cudaSuccess) rc = SCAN_ERR_CUDA;
+    cudaStreamWaitEvent(s_in, ev_start, 0);
+    cudaStreamWaitEvent(s_out, ev_start, 0);
+    if (cudaMemsetAsync(trip, 0, 24, s_c) != cudaSuccess) rc = SCAN_ERR_CUDA;  // carry_0 = 0
+    auto h2d = [&](int64_t i) {
+        const int64_t off = i * chunk_elems, cnt = n - off < chunk_elems ? n - off : chunk_elems;
+        if (i >= 2) cudaStreamWaitEvent(s_in, ev_comp[i & 1], 0);  // scan of chunk i-2 has read the buffer
+        cudaMemcpyAsync(d_in[i & 1], (const uint8_t*)h_in + off * isz, cnt * isz, cudaMemcpyHostToDevice, s_in);
+        cudaEventRecord(ev_in[i & 1], s_in);
+    };
+    h2d(0);
+    for (int64_t i = 0; i < nchunks && rc == SCAN_OK; ++i) {
+        if (i + 1 < nchunks) h2d(i + 1);
+        const int64_t off = i * chunk_elems, cnt = n - off < chunk_elems ? n - off : chunk_elems;
+        cudaStreamWaitEvent(s_c, ev_in[i & 1], 0);
+        if (i >= 2) cudaStreamWaitEvent(s_c, ev_out[i & 1], 0);  // d_out[i&1] copied out
+        uint8_t* tr = trip + 24 * (i % 3);
+        uint8_t* tr_next = trip + 24 * ((i + 1) % 3);
+        rc = scan_1d(d_in[i & 1], d_out[i & 1], cnt, dtype, tr, ws, ws_bytes, stream, exclusive);
+        if (rc == SCAN_OK && i + 1 < nchunks) {
+            rc = scan_total(d_in[i & 1], cnt, dtype, tr + 8, ws, ws_bytes, stream);       // total_i
+            if (rc == SCAN_OK) rc = scan_carry_from_totals(tr, 3, 2, dtype, tr_next, stream);  // carry + total
+        }
+        cudaEventRecord(ev_comp[i & 1], s_c);
+        cudaStreamWaitEvent(s_out, ev_comp[i & 1], 0);
+        cudaMemcpyAsync((uint8_t*)h_out + off * 4, d_out[i & 1], cnt * 4, cudaMemcpyDeviceToHost, s_out);
+        cudaEventRecord(ev_out[i & 1], s_out);
+    }
+    // the caller's stream resumes after the last copy out
+    cudaStreamWaitEvent(s_c, ev_out[(nchunks - 1) & 1], 0);
+    if (nchunks >= 2) cudaStreamWaitEvent(s_c, ev_out[(nchunks - 2) & 1], 0);
+    cudaEventDestroy(ev_start);
+    for (int k = 0; k < 2; ++k) {
+        cudaEventDestroy(ev_in[k]);
+        cudaEventDestroy(ev_comp[k]);
+        cudaEventDestroy(ev_out[k]);
+    }
+    if (rc == SCAN_OK && cudaGetLastError() != cudaSuccess) rc = SCAN_ERR_CUDA;
+    return rc;
+}
+
 }  // extern "C"

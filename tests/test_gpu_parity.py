@@ -300,3 +300,19 @@ def test_rows_many_tiles_strided(cuda, oracle, inputs_mod, dt):
         torch.cuda.synchronize()
         for r in range(R):
             assert_parity(oracle, out[r], oracle_1d(oracle, np.ascontiguousarray(x[r, :C]), dt, exc), dt)
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+def test_host_streaming(cuda, oracle, inputs_mod, dt):
+    """scan_host: pinned host in -> chunked H2D / scan / D2H pipeline -> host out,
+    with ragged chunk counts (carry chained across chunks on the device)."""
+    n = 5 * (1 << 20) + 777
+    x = host_input(inputs_mod, dt, n, seed=31)
+    t = torch.from_numpy(x)
+    if dt == "f16":
+        t = t.view(torch.float16)
+    h = t.pin_memory()
+    for exc, chunk in ((False, 1 << 20), (True, 3 * (1 << 19) + 5), (False, n)):
+        got = cuda.host_scan(h, exclusive=exc, chunk=chunk)
+        torch.cuda.synchronize()
+        assert_parity(oracle, got, oracle_1d(oracle, x, dt, exc), dt)
