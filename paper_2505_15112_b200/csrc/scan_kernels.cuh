@@ -706,9 +706,48 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
 }
 
 // ---------------------------------------------------------------- reduction
-// scan_total: fixed partition of [0, n) into gridDim.x contiguous chunks;
-// per-thread sums in int64 / fp64, block reduction, then the last CTA adds
-// the per-CTA partials in index order (deterministic).
+// scan_total: fixed partition of [0, n) into gridDim.x contiguous chunks; each
+// thread streams 16-byte vectors (4-deep, so ~64 B per thread are in flight)
+// of its chunk in a fixed order, widening every element exactly to int64 /
+// fp64 (so |error| <= n 2^-53 sum|x| for floats); then a fixed-order block reduction, and the
+// last CTA adds the per-CTA partials in index order (identical bits per call).
+template <typename In>
+struct Vec16;
+template <> struct Vec16<int32_t> { static constexpr int kN = 4; };
+template <> struct Vec16<float> { static constexpr int kN = 4; };
+template <> struct Vec16<uint16_t> { static constexpr int kN = 8; };
+template <> struct Vec16<int8_t> { static constexpr int kN = 16; };
+
+template <typename Sum>
+__device__ __forceinline__ Sum to_sum(uint32_t x) { return (Sum)(int32_t)x; }  // ints: sign of the wrap type
+template <typename Sum>
+__device__ __forceinline__ Sum to_sum(float x) { return (Sum)x; }
+
+template <int DT, typename Sum>
+__device__ __forceinline__ Sum sum_vec16(const uint4& q)
+{
+    using In = typename Traits<DT>::In;
+    constexpr int N = Vec16<In>::kN;
+    if constexpr (sizeof(In) == 1) {
+        // 16 signed bytes: four dp4a (4-way byte dot product with 1,1,1,1)
+        int t = __dp4a((int)q.x, 0x01010101, 0);
+        t = __dp4a((int)q.y, 0x01010101, t);
+        t = __dp4a((int)q.z, 0x01010101, t);
+        t = __dp4a((int)q.w, 0x01010101, t);
+        return (Sum)t;
+    }
+    const In* e = reinterpret_cast<const In*>(&q);
+    Sum s = 0;
+#pragma unroll
+    for (int k = 0; k < N; k += 2) {
+        if constexpr (Traits<DT>::kFloat)
+            s += (double)widen(e[k]) + (double)widen(e[k + 1]);  // every element widened exactly to fp64
+        else
+            s += (long long)(int32_t)widen(e[k]) + (long long)(int32_t)widen(e[k + 1]);
+    }
+    return s;
+}
+
 template <int DT, int THREADS>
 __global__ void __launch_bounds__(THREADS) k_total(const void* in_, int64_t n, void* total_out,
                                                    uint8_t* ws)
@@ -716,20 +755,37 @@ __global__ void __launch_bounds__(THREADS) k_total(const void* in_, int64_t n, v
     using Tr = Traits<DT>;
     using In = typename Tr::In;
     using Sum = typename std::conditional<Tr::kFloat, double, long long>::type;
+    constexpr int VN = Vec16<In>::kN;
     const In* in = reinterpret_cast<const In*>(in_);
     WsHeader* hdr = reinterpret_cast<WsHeader*>(ws);
     Sum* partials = reinterpret_cast<Sum*>(ws + kWsPartialsOffset);
 
-    int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
-    int64_t lo = (int64_t)blockIdx.x * chunk;
-    int64_t hi = lo + chunk < n ? lo + chunk : n;
+    // chunk boundaries in whole 16-byte vectors (the unaligned head goes to CTA 0,
+    // the tail past the last whole vector to the last CTA)
+    const int64_t head = (int64_t)((16 - ((uintptr_t)in & 15)) & 15) / (int64_t)sizeof(In);
+    const int64_t h = head < n ? head : n;
+    const int64_t nvec = (n - h) / VN;
+    const uint4* vin = reinterpret_cast<const uint4*>(in + h);
+    const int64_t vchunk = (nvec + gridDim.x - 1) / gridDim.x;
+    const int64_t vlo = (int64_t)blockIdx.x * vchunk;
+    const int64_t vhi = vlo + vchunk < nvec ? vlo + vchunk : nvec;
     Sum acc = 0;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += THREADS) {
-        if constexpr (Tr::kFloat)
-            acc += (double)widen(in[i]);
-        else
-            acc += (long long)(int32_t)widen(in[i]);
+    int64_t i = vlo + threadIdx.x;
+    for (; i + 3 * THREADS < vhi; i += 4 * THREADS) {
+        const uint4 a = ptx::ld_stream_v4(vin + i);
+        const uint4 b = ptx::ld_stream_v4(vin + i + THREADS);
+        const uint4 c = ptx::ld_stream_v4(vin + i + 2 * THREADS);
+        const uint4 d = ptx::ld_stream_v4(vin + i + 3 * THREADS);
+        acc += sum_vec16<DT, Sum>(a);
+        acc += sum_vec16<DT, Sum>(b);
+        acc += sum_vec16<DT, Sum>(c);
+        acc += sum_vec16<DT, Sum>(d);
     }
+    for (; i < vhi; i += THREADS) acc += sum_vec16<DT, Sum>(ptx::ld_stream_v4(vin + i));
+    if (blockIdx.x == 0)
+        for (int64_t j = threadIdx.x; j < h; j += THREADS) acc += to_sum<Sum>(widen(in[j]));
+    if (blockIdx.x == gridDim.x - 1)
+        for (int64_t j = h + nvec * VN + threadIdx.x; j < n; j += THREADS) acc += to_sum<Sum>(widen(in[j]));
     // block reduction (fixed order)
     __shared__ Sum s_part[THREADS / 32];
 #pragma unroll
