@@ -168,6 +168,16 @@ __device__ __forceinline__ void named_bar_sync(int id, int count)
 }
 
 // ---- streaming global loads (non-TMA paths) ---------------------------------------
+// 16-byte read-only load kept in L2 with the given policy (e.g. evict_last).
+__device__ __forceinline__ uint4 ld_keep_v4(const void* p, uint64_t policy)
+{
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p), "l"(policy));
+    return r;
+}
+
 __device__ __forceinline__ uint4 ld_stream_v4(const void* p)
 {
     uint4 r;

@@ -706,8 +706,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
 }
 
 // ---------------------------------------------------------------- reduction
-// scan_total: fixed partition of [0, n) into gridDim.x contiguous chunks; each
-// thread streams 16-byte vectors (4-deep, so ~64 B per thread are in flight)
+// scan_total: every thread streams 16-byte vectors (4-deep, so ~64 B per thread are in flight)
 // of its chunk in a fixed order, widening every element exactly to int64 /
 // fp64 (so |error| <= n 2^-53 sum|x| for floats); then a fixed-order block reduction, and the
 // last CTA adds the per-CTA partials in index order (identical bits per call).
@@ -766,22 +765,25 @@ __global__ void __launch_bounds__(THREADS) k_total(const void* in_, int64_t n, v
     const int64_t h = head < n ? head : n;
     const int64_t nvec = (n - h) / VN;
     const uint4* vin = reinterpret_cast<const uint4*>(in + h);
-    const int64_t vchunk = (nvec + gridDim.x - 1) / gridDim.x;
-    const int64_t vlo = (int64_t)blockIdx.x * vchunk;
-    const int64_t vhi = vlo + vchunk < nvec ? vlo + vchunk : nvec;
+    // Grid-stride BACKWARDS from the end of the array with an L2 evict_last
+    // hint: the bytes read last are the array's beginning, which the scan
+    // that follows (multi-GPU RSS: total, then scan of the same shard) reads
+    // first -- up to ~100 MB of the shard is then served by L2, not HBM.
+    const uint64_t pol = ptx::policy_evict_last();
+    const int64_t T = (int64_t)gridDim.x * THREADS;
     Sum acc = 0;
-    int64_t i = vlo + threadIdx.x;
-    for (; i + 3 * THREADS < vhi; i += 4 * THREADS) {
-        const uint4 a = ptx::ld_stream_v4(vin + i);
-        const uint4 b = ptx::ld_stream_v4(vin + i + THREADS);
-        const uint4 c = ptx::ld_stream_v4(vin + i + 2 * THREADS);
-        const uint4 d = ptx::ld_stream_v4(vin + i + 3 * THREADS);
+    int64_t i = nvec - 1 - ((int64_t)blockIdx.x * THREADS + threadIdx.x);
+    for (; i - 3 * T >= 0; i -= 4 * T) {
+        const uint4 a = ptx::ld_keep_v4(vin + i, pol);
+        const uint4 b = ptx::ld_keep_v4(vin + i - T, pol);
+        const uint4 c = ptx::ld_keep_v4(vin + i - 2 * T, pol);
+        const uint4 d = ptx::ld_keep_v4(vin + i - 3 * T, pol);
         acc += sum_vec16<DT, Sum>(a);
         acc += sum_vec16<DT, Sum>(b);
         acc += sum_vec16<DT, Sum>(c);
         acc += sum_vec16<DT, Sum>(d);
     }
-    for (; i < vhi; i += THREADS) acc += sum_vec16<DT, Sum>(ptx::ld_stream_v4(vin + i));
+    for (; i >= 0; i -= T) acc += sum_vec16<DT, Sum>(ptx::ld_keep_v4(vin + i, pol));
     if (blockIdx.x == 0)
         for (int64_t j = threadIdx.x; j < h; j += THREADS) acc += to_sum<Sum>(widen(in[j]));
     if (blockIdx.x == gridDim.x - 1)
