@@ -53,29 +53,30 @@ constexpr int kMcProf = 18;
 
 // Block reductions live in the workspace after the header: r[c][b] (8 bytes
 // each, chunk-major); barrier counters in their own region (kWsBarOffset).
+// Geometry in TILE units (32-bit: n <= 2^32 elements is <= 2^19 tiles).
 struct McGeom {
     int64_t n;          // elements
-    int64_t tile;       // elements per tile
-    int64_t bt;         // tiles per block
-    int64_t block;      // elements per block = bt * tile
-    int64_t chunk;      // elements per chunk = G * block
-    int64_t chunks;     // number of chunks
+    int ntiles;         // ceil(n / TILE)
+    int full_tiles;     // tiles [0, full_tiles) are whole and inside both TMA views
+    int bt;             // tiles per block
+    int chunk_tiles;    // g * bt
+    int chunks;         // number of chunks
     int g;              // CTAs (blocks per chunk)
 };
 
 // Job q of a CTA's sequence with reductions running `ahead` chunks ahead of
 // scans: R(0)..R(ahead), then S(0) R(ahead+1) S(1) R(ahead+2) ..., then the
 // remaining S jobs.  Returns the chunk and whether it is a scan (S) job.
-__device__ __forceinline__ void mc_job(int64_t q, int64_t chunks, int ahead, int64_t& c, bool& is_scan)
+__device__ __forceinline__ void mc_job(int q, int chunks, int ahead, int& c, bool& is_scan)
 {
-    const int64_t F = chunks < ahead + 1 ? chunks : ahead + 1;  // leading reductions
+    const int F = chunks < ahead + 1 ? chunks : ahead + 1;  // leading reductions
     if (q < F) {
         c = q;
         is_scan = false;
         return;
     }
-    const int64_t qq = q - F;
-    const int64_t P = chunks - F;                                  // (S, R) pairs
+    const int qq = q - F;
+    const int P = chunks - F;  // (S, R) pairs
     if (qq < 2 * P) {
         c = (qq & 1) ? (qq >> 1) + F : (qq >> 1);
         is_scan = (qq & 1) == 0;
@@ -84,6 +85,22 @@ __device__ __forceinline__ void mc_job(int64_t q, int64_t chunks, int ahead, int
         is_scan = true;
     }
 }
+
+// Ring position: slot index and the parity of its current use.
+template <int NB>
+struct Ring {
+    int s = 0;
+    uint32_t ph = 0;
+    bool wrapped = false;  // true once every slot has been used at least once
+    __device__ __forceinline__ void next()
+    {
+        if (++s == NB) {
+            s = 0;
+            ph ^= 1u;
+            wrapped = true;
+        }
+    }
+};
 
 struct McParams16 {
     CUtensorMap tm_in;      // 2-D [rows x 128 B] view of the input (unused for int8)
@@ -160,43 +177,193 @@ __device__ __forceinline__ uint32_t swz_elem(int e)
     }
 }
 
-__device__ __forceinline__ void load16(const uint8_t* slot, int e0, uint32_t (&v)[16], const int32_t*)
+// ---- one lane's group of 16 contiguous elements, as raw input words ------------
+// SZ = sizeof(In): 16 words (4-byte), 8 words (fp16 pairs) or 4 words (int8 quads).
+template <int SZ>
+struct Grp {
+    uint32_t w[4 * SZ];
+};
+
+// Full group from a swizzled (4-/2-byte) or linear (1-byte) ring slot.
+template <int SZ>
+__device__ __forceinline__ void grp_load(const uint8_t* slot, int e0, Grp<SZ>& g)
 {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const uint4 q = *reinterpret_cast<const uint4*>(slot + swz4(e0, j));
-        v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+    for (int j = 0; j < SZ; ++j) {
+        uint32_t off;
+        if constexpr (SZ == 4) off = swz4(e0, j);
+        else if constexpr (SZ == 2) off = swz2(e0, j);
+        else off = (uint32_t)e0;
+        const uint4 q = *reinterpret_cast<const uint4*>(slot + off);
+        g.w[4 * j] = q.x; g.w[4 * j + 1] = q.y; g.w[4 * j + 2] = q.z; g.w[4 * j + 3] = q.w;
     }
 }
-__device__ __forceinline__ void load16(const uint8_t* slot, int e0, float (&v)[16], const float*)
+
+// Ragged group: element e0+k is read from the slot below m_tma, from global
+// memory below m, and is 0 (the identity) beyond.
+template <int SZ>
+__device__ __forceinline__ uint32_t raw_bits(const void* p)
+{
+    if constexpr (SZ == 4) return *reinterpret_cast<const uint32_t*>(p);
+    else if constexpr (SZ == 2) return *reinterpret_cast<const uint16_t*>(p);
+    else return *reinterpret_cast<const uint8_t*>(p);
+}
+template <int SZ>
+__device__ __forceinline__ void grp_load_tail(const uint8_t* slot, const uint8_t* gin_tile, int e0, int m,
+                                              int m_tma, Grp<SZ>& g)
 {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const float4 q = *reinterpret_cast<const float4*>(slot + swz4(e0, j));
-        v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+    for (int j = 0; j < 4 * SZ; ++j) g.w[j] = 0u;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int e = e0 + k;
+        uint32_t bits = 0u;
+        if (e < m_tma) bits = raw_bits<SZ>(slot + swz_elem<SZ>(e));
+        else if (e < m) bits = raw_bits<SZ>(gin_tile + (size_t)e * SZ);
+        g.w[(k * SZ) / 4] |= bits << ((k * SZ * 8) & 31);
     }
 }
-__device__ __forceinline__ void load16(const uint8_t* slot, int e0, float (&v)[16], const uint16_t*)
+
+// fp16 (raw binary16 in the low / high half of w) + fp32 -> fp32 with ONE
+// rounding: sm_100's mixed-precision add (SASS FHADD, .H1 operand select), so
+// widening costs no instruction of its own.
+__device__ __forceinline__ float fhadd_lo(uint32_t w, float c)
 {
+    float d;
+    asm("{.reg .f16 l, h; mov.b32 {l, h}, %1; add.rn.f32.f16 %0, l, %2;}" : "=f"(d) : "r"(w), "f"(c));
+    return d;
+}
+__device__ __forceinline__ float fhadd_hi(uint32_t w, float c)
+{
+    float d;
+    asm("{.reg .f16 l, h; mov.b32 {l, h}, %1; add.rn.f32.f16 %0, h, %2;}" : "=f"(d) : "r"(w), "f"(c));
+    return d;
+}
+
+// int8: c + (signed byte sum of w selected by mask), exact mod 2^32 (IDP.4A).
+__device__ __forceinline__ uint32_t dp4(uint32_t w, uint32_t mask, uint32_t c)
+{
+    return (uint32_t)__dp4a((int)w, (int)mask, (int)c);
+}
+
+// Reduction of a group (Phase I).  Floats: fp32 partials, widened to the fp64 carry.
+__device__ __forceinline__ uint32_t grp_sum(const Grp<4>& g, const int32_t*)
+{
+    uint32_t s[4];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const uint4 q = *reinterpret_cast<const uint4*>(slot + swz2(e0, j));
-        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+    for (int j = 0; j < 4; ++j) s[j] = (g.w[4 * j] + g.w[4 * j + 1]) + (g.w[4 * j + 2] + g.w[4 * j + 3]);
+    return (s[0] + s[1]) + (s[2] + s[3]);
+}
+__device__ __forceinline__ double grp_sum(const Grp<4>& g, const float*)
+{
+    float s8[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[k]));
-            v[8 * j + 2 * k] = f.x;
-            v[8 * j + 2 * k + 1] = f.y;
+    for (int k = 0; k < 8; ++k) s8[k] = __uint_as_float(g.w[2 * k]) + __uint_as_float(g.w[2 * k + 1]);
+    const float a = (s8[0] + s8[1]) + (s8[2] + s8[3]);
+    const float b = (s8[4] + s8[5]) + (s8[6] + s8[7]);
+    return (double)(a + b);
+}
+__device__ __forceinline__ double grp_sum(const Grp<2>& g, const uint16_t*)
+{
+    float a = -0.0f, b = -0.0f;  // two independent FHADD chains (elements 0-7, 8-15)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        a = fhadd_hi(g.w[j], fhadd_lo(g.w[j], a));
+        b = fhadd_hi(g.w[4 + j], fhadd_lo(g.w[4 + j], b));
+    }
+    return (double)(a + b);
+}
+__device__ __forceinline__ uint32_t grp_sum(const Grp<1>& g, const int8_t*)
+{
+    uint32_t s = 0u;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s = dp4(g.w[j], 0x01010101u, s);
+    return s;
+}
+
+// In-lane inclusive prefix v[k] = x_0 + ... + x_k (4- and 2-byte inputs).
+__device__ __forceinline__ void grp_prefix(const Grp<4>& g, uint32_t (&v)[16], const int32_t*)
+{
+    v[0] = g.w[0];
+#pragma unroll
+    for (int k = 1; k < 16; ++k) v[k] = v[k - 1] + g.w[k];
+}
+__device__ __forceinline__ void grp_prefix(const Grp<4>& g, float (&v)[16], const float*)
+{
+    v[0] = __uint_as_float(g.w[0]);
+#pragma unroll
+    for (int k = 1; k < 16; ++k) v[k] = v[k - 1] + __uint_as_float(g.w[k]);
+}
+__device__ __forceinline__ void grp_prefix(const Grp<2>& g, float (&v)[16], const uint16_t*)
+{
+    v[0] = fhadd_lo(g.w[0], -0.0f);  // exact widening (x + -0 == x, -0 kept)
+    v[1] = fhadd_hi(g.w[0], v[0]);
+#pragma unroll
+    for (int j = 1; j < 8; ++j) {
+        v[2 * j] = fhadd_lo(g.w[j], v[2 * j - 1]);
+        v[2 * j + 1] = fhadd_hi(g.w[j], v[2 * j]);
+    }
+}
+
+// int8 epilogue straight from the raw bytes: out = base + prefix of the bytes,
+// one IDP.4A per element (masks select bytes 0..k of the word).
+__device__ __forceinline__ void grp_emit_i8(const Grp<1>& g, uint32_t B, bool exclusive, uint32_t (&o)[16])
+{
+    uint32_t b = B;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (exclusive) {
+            o[4 * j] = b;
+            o[4 * j + 1] = dp4(g.w[j], 0x00000001u, b);
+            o[4 * j + 2] = dp4(g.w[j], 0x00000101u, b);
+            o[4 * j + 3] = dp4(g.w[j], 0x00010101u, b);
+            b = dp4(g.w[j], 0x01010101u, b);
+        } else {
+            o[4 * j] = dp4(g.w[j], 0x00000001u, b);
+            o[4 * j + 1] = dp4(g.w[j], 0x00000101u, b);
+            o[4 * j + 2] = dp4(g.w[j], 0x00010101u, b);
+            o[4 * j + 3] = dp4(g.w[j], 0x01010101u, b);
+            b = o[4 * j + 3];
         }
     }
 }
-__device__ __forceinline__ void load16(const uint8_t* slot, int e0, uint32_t (&v)[16], const int8_t*)
-{
-    const uint4 q = *reinterpret_cast<const uint4*>(slot + e0);
-    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+
+// One lane's 16 elements through a tile scan: load raw words, form the lane
+// total (int8: IDP.4A byte sums; others: the in-lane inclusive prefix v), then
+// emit base + local prefix.  Used by k_mcscan16 and k_rowscan16.
+template <int DT>
+struct LaneScan {
+    using Tr = Traits<DT>;
+    using In = typename Tr::In;
+    using Acc = typename Tr::Acc;
+    static constexpr int SZ = (int)sizeof(In);
+    static constexpr bool kBytes = SZ == 1;
+    Grp<SZ> g;
+    Acc v[kBytes ? 1 : 16];
+
+    __device__ __forceinline__ Acc prefix()
+    {
+        if constexpr (kBytes) {
+            return grp_sum(g, (const In*)nullptr);
+        } else {
+            grp_prefix(g, v, (const In*)nullptr);
+            return v[15];
+        }
+    }
+    __device__ __forceinline__ void emit(Acc B, bool exclusive, Acc (&o)[16]) const
+    {
+        if constexpr (kBytes) {
+            grp_emit_i8(g, B, exclusive, o);
+        } else if (exclusive) {
+            o[0] = B;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = (uint32_t)(int32_t)(int8_t)(w[k >> 2] >> (8 * (k & 3)));
-}
+            for (int k = 1; k < 16; ++k) o[k] = B + v[k - 1];
+        } else {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) o[k] = B + v[k];
+        }
+    }
+};
 
 template <typename A>
 __device__ __forceinline__ void store16(uint8_t* slot, int e0, const A (&o)[16])
@@ -233,6 +400,48 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, int x, int y
                  : "memory");
 }
 
+// Per-lane byte offsets of the 16-byte chunks of a lane's group 0 inside a
+// ring slot; group g of the same lane sits g * kGrp bytes further (the
+// swizzle phase R & 7 is the same for every group, 512 elements apart).
+template <int SZ>
+struct LaneOffsets {
+    static constexpr uint32_t kGrpIn = SZ == 4 ? 2048u : (SZ == 2 ? 1024u : 512u);
+    static constexpr uint32_t kGrpOut = 2048u;
+    uint32_t in[SZ];
+    uint32_t out[4];
+    __device__ __forceinline__ explicit LaneOffsets(int e0)
+    {
+#pragma unroll
+        for (int j = 0; j < SZ; ++j) in[j] = SZ == 4 ? swz4(e0, j) : (SZ == 2 ? swz2(e0, j) : (uint32_t)e0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) out[j] = swz4(e0, j);
+    }
+};
+
+template <int SZ>
+__device__ __forceinline__ void grp_load_off(const uint8_t* base, const uint32_t (&off)[SZ], Grp<SZ>& g)
+{
+#pragma unroll
+    for (int j = 0; j < SZ; ++j) {
+        const uint4 q = *reinterpret_cast<const uint4*>(base + off[j]);
+        g.w[4 * j] = q.x; g.w[4 * j + 1] = q.y; g.w[4 * j + 2] = q.z; g.w[4 * j + 3] = q.w;
+    }
+}
+
+template <typename A>
+__device__ __forceinline__ void store16_off(uint8_t* base, const uint32_t (&off)[4], const A (&o)[16])
+{
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        uint4 q;
+        q.x = *reinterpret_cast<const uint32_t*>(&o[4 * j]);
+        q.y = *reinterpret_cast<const uint32_t*>(&o[4 * j + 1]);
+        q.z = *reinterpret_cast<const uint32_t*>(&o[4 * j + 2]);
+        q.w = *reinterpret_cast<const uint32_t*>(&o[4 * j + 3]);
+        *reinterpret_cast<uint4*>(base + off[j]) = q;
+    }
+}
+
 template <int DT, int NC, int GPW, int NB_IN, int NB_OUT>
 __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_constant__ McParams16 p)
 {
@@ -243,6 +452,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     using Acc = typename Tr::Acc;
     using Carry = typename Tr::Carry;
     constexpr int TILE = Cfg::kTile;
+    constexpr int SZ = (int)sizeof(In);
     constexpr int KC = 4;
     constexpr int RS = 4;  // reduce-sum hand-off ring (ahead <= 2)
 
@@ -259,7 +469,6 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     __shared__ __align__(8) uint64_t out_empty[NSR];
     __shared__ __align__(8) uint64_t carry_ready[KC];
     __shared__ __align__(8) uint64_t rsum_ready[RS];
-    __shared__ int64_t s_store_g0[NSR];
     __shared__ Acc s_wt[2][NC];
     __shared__ Carry s_job_sum[RS][NC];
     __shared__ Carry s_carry[KC];
@@ -270,7 +479,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     const int warp = tid >> 5;
     const McGeom& gm = p.gm;
     const int b = blockIdx.x;
-    const int64_t njobs = gm.chunks * 2;
+    const int njobs = gm.chunks * 2;
     const bool prof = (p.debug & 4) != 0;
     const long long t_start = clock64();
 
@@ -296,11 +505,12 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     }
     __syncthreads();
 
-    auto block_range = [&](int64_t c, int64_t& lo, int64_t& hi) {
-        lo = c * gm.chunk + (int64_t)b * gm.block;
-        hi = lo + gm.block;
-        if (lo > gm.n) lo = gm.n;
-        if (hi > gm.n) hi = gm.n;
+    // Tiles [t0, t1) of block b of chunk c.
+    auto block_tiles = [&](int c, int& t0, int& t1) {
+        t0 = c * gm.chunk_tiles + b * gm.bt;
+        t1 = t0 + gm.bt;
+        if (t0 > gm.ntiles) t0 = gm.ntiles;
+        if (t1 > gm.ntiles) t1 = gm.ntiles;
     };
 
     if (warp == 0) {
@@ -308,35 +518,33 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         if (lane == 0) {
             const uint64_t pol_keep = ptx::policy_evict_last();
             const uint64_t pol_drop = ptx::policy_evict_first();
-            int64_t q_tile = 0;
-            for (int64_t q = 0; q < njobs; ++q) {
-                int64_t c;
+            Ring<NB_IN> rin;
+            for (int q = 0; q < njobs; ++q) {
+                int c, t0, t1;
                 bool is_scan;
                 mc_job(q, gm.chunks, p.ahead, c, is_scan);
-                int64_t lo, hi;
-                block_range(c, lo, hi);
-                for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++q_tile) {
-                    const int s = (int)(q_tile % NB_IN);
-                    const uint32_t use = (uint32_t)(q_tile / NB_IN);
-                    if (use > 0) ptx::mbar_wait(&in_empty[s], (use - 1) & 1u);
-                    uint8_t* dst = in_ring + s * Cfg::kRingSlot;
-                    const uint64_t pol = is_scan ? pol_drop : pol_keep;
-                    if constexpr (sizeof(In) == 1) {
+                block_tiles(c, t0, t1);
+                const uint64_t pol = is_scan ? pol_drop : pol_keep;
+                for (int t = t0; t < t1; ++t, rin.next()) {
+                    if (rin.wrapped) ptx::mbar_wait(&in_empty[rin.s], rin.ph ^ 1u);
+                    uint8_t* dst = in_ring + rin.s * Cfg::kRingSlot;
+                    if constexpr (SZ == 1) {
+                        const int64_t g0 = (int64_t)t * TILE;
                         int64_t m_tma = p.n_tma_in - g0;
                         m_tma = m_tma < 0 ? 0 : (m_tma > TILE ? TILE : m_tma);
                         if (m_tma > 0) {
-                            ptx::mbar_arrive_expect_tx(&in_full[s], (uint32_t)m_tma);
-                            ptx::tma_load_1d(dst, gin + g0, (uint32_t)m_tma, &in_full[s], pol);
+                            ptx::mbar_arrive_expect_tx(&in_full[rin.s], (uint32_t)m_tma);
+                            ptx::tma_load_1d(dst, gin + g0, (uint32_t)m_tma, &in_full[rin.s], pol);
                         } else {
-                            ptx::mbar_arrive(&in_full[s]);
+                            ptx::mbar_arrive(&in_full[rin.s]);
                         }
                     } else {
-                        ptx::mbar_arrive_expect_tx(&in_full[s], (uint32_t)Cfg::kInSlot);
-                        const int y0 = (int)(g0 / Cfg::kRowElemsIn);
+                        ptx::mbar_arrive_expect_tx(&in_full[rin.s], (uint32_t)Cfg::kInSlot);
+                        const int y0 = t * (TILE / Cfg::kRowElemsIn);
 #pragma unroll
                         for (int k = 0; k < Cfg::kBoxesIn; ++k)
                             tma_load_2d(dst + k * Cfg::kBoxRowsIn * 128, &p.tm_in, 0, y0 + Cfg::kBoxRowsIn * k,
-                                        &in_full[s], pol);
+                                        &in_full[rin.s], pol);
                     }
                 }
             }
@@ -345,8 +553,9 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         // =========================== storer ===========================
         if (lane == 0) {
             const uint64_t pol = ptx::policy_evict_first();
-            int64_t o_tile = 0, q_tile = 0;
-            uint32_t sparity = 0;  // UNI: bit s = parity of the next store_ready[s] phase
+            Ring<NB_IN> rin;    // UNI: outputs sit in the input slots
+            Ring<NSR> rout;
+            uint32_t sparity = 0;  // UNI: bit s = parity of the next store_ready[s] phase (S tiles only)
             int pend = -1;         // slot whose store may still be reading shared memory
             auto release = [&](int slot) {
                 if (UNI)
@@ -354,19 +563,19 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 else
                     ptx::mbar_arrive(&out_empty[slot]);
             };
-            for (int64_t q = 0; q < njobs; ++q) {
-                int64_t c;
+            for (int q = 0; q < njobs; ++q) {
+                int c, t0, t1;
                 bool is_scan;
                 mc_job(q, gm.chunks, p.ahead, c, is_scan);
-                int64_t lo, hi;
-                block_range(c, lo, hi);
+                block_tiles(c, t0, t1);
                 if (!is_scan) {
-                    if (UNI) q_tile += (hi - lo + TILE - 1) / TILE;
+                    if (UNI)
+                        for (int t = t0; t < t1; ++t) rin.next();
                     continue;
                 }
-                for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++o_tile, ++q_tile) {
-                    const int o = UNI ? (int)(q_tile % NB_IN) : (int)(o_tile % NB_OUT);
-                    const uint32_t par = UNI ? ((sparity >> o) & 1u) : (uint32_t)(o_tile / NB_OUT) & 1u;
+                for (int t = t0; t < t1; ++t, rin.next(), rout.next()) {
+                    const int o = UNI ? rin.s : rout.s;
+                    const uint32_t par = UNI ? ((sparity >> o) & 1u) : rout.ph;
                     if (pend >= 0 && !ptx::mbar_try_wait(&store_ready[o], par)) {
                         // about to block: release the pending slot first
                         ptx::bulk_wait_read<0>();
@@ -375,8 +584,8 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     }
                     mbar_wait_prof(&store_ready[o], par, prof, &s_prof[5]);
                     if (UNI) sparity ^= 1u << o;
-                    if (g0 < p.n_tma_out) {
-                        const int y0 = (int)(g0 / 32);
+                    if ((int64_t)t * TILE < p.n_tma_out) {
+                        const int y0 = t * (TILE / 32);
 #pragma unroll
                         for (int k = 0; k < Cfg::kBoxesOut; ++k)
                             tma_store_2d(&p.tm_out, 0, y0 + Cfg::kBoxRowsOut * k,
@@ -411,7 +620,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         // chunk barrier), and form the carry of chunk c as soon as its barrier
         // is complete (SyncAll P245; partial = sum of the first b entries of r,
         // P248) -- whichever is ready first, so neither waits on the other.
-        int64_t next_pub = 0, next_car = 0;
+        int next_pub = 0, next_car = 0;
         uint32_t backoff = 32;
         long long spin0 = 0;
         while (next_car < gm.chunks) {
@@ -421,7 +630,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 if (lane == 0) {
                     Carry t = Carry(0);
                     for (int w = 0; w < NC; ++w) t = t + s_job_sum[next_pub % RS][w];
-                    r_all[next_pub * gm.g + b] = carry_bits(t);
+                    r_all[(int64_t)next_pub * gm.g + b] = carry_bits(t);
                     ptx::red_release_add_u32(&bar[next_pub], 1u);  // orders the r store before the arrival
                 }
                 __syncwarp();
@@ -432,12 +641,12 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 uint32_t arrived = lane == 0 ? ld_acquire_u32(&bar[next_car]) : 0u;
                 arrived = __shfl_sync(0xffffffffu, arrived, 0);
                 if (arrived >= (uint32_t)gm.g) {
-                    const int64_t c = next_car;
+                    const int c = next_car;
                     uint64_t rb[RPL];
 #pragma unroll
                     for (int k = 0; k < RPL; ++k) {
                         const int bb = lane + 32 * k;
-                        rb[k] = bb < gm.g ? ld_relaxed_u64(&r_all[c * gm.g + bb]) : 0ull;
+                        rb[k] = bb < gm.g ? ld_relaxed_u64(&r_all[(int64_t)c * gm.g + bb]) : 0ull;
                     }
                     Carry below = Carry(0), total = Carry(0);
 #pragma unroll
@@ -473,60 +682,57 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     } else {
         // =========================== compute ===========================
         const int cw = warp - 3;
-        int64_t q_tile = 0, o_tile = 0, s_count = 0;
+        const int e0_base = cw * GPW * 512 + 16 * lane;  // group g: + 512 g
+        const LaneOffsets<SZ> off(e0_base);
+        constexpr uint32_t GI = LaneOffsets<SZ>::kGrpIn, GO = LaneOffsets<SZ>::kGrpOut;
+        const uint8_t* const gin_b = reinterpret_cast<const uint8_t*>(p.in);
+        const bool exclusive = p.exclusive != 0;
+        const bool prof0 = prof && cw == 0 && lane == 0;
+        Ring<NB_IN> rin;
+        Ring<NSR> rout;  // !UNI only
+        int s_count = 0;
 
-        // 16 elements of tile-offset e0 (valid m, TMA-covered m_tma) into v.
-        auto load_lane = [&](const uint8_t* slot, int64_t g0, int e0, int m, int m_tma, Acc (&v)[16]) {
-            if (e0 + 16 <= m_tma) {
-                load16(slot, e0, v, (const In*)nullptr);
-            } else {
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const int e = e0 + k;
-                    if (e < m_tma)
-                        v[k] = widen(*reinterpret_cast<const In*>(slot + swz_elem<sizeof(In)>(e)));
-                    else if (e < m)
-                        v[k] = widen(gin[g0 + e]);
-                    else
-                        v[k] = Acc(0);
-                }
-            }
+        // Valid elements m and TMA-covered elements m_tma of a ragged tile t.
+        auto ragged = [&](int t, int& m, int& m_in, int& m_out) {
+            const int64_t g0 = (int64_t)t * TILE;
+            const int64_t r = gm.n - g0, ri = p.n_tma_in - g0, ro = p.n_tma_out - g0;
+            m = (int)(r < TILE ? r : TILE);
+            m_in = (int)(ri < 0 ? 0 : (ri > m ? m : ri));
+            m_out = (int)(ro < 0 ? 0 : (ro > m ? m : ro));
         };
 
-        for (int64_t q = 0; q < njobs; ++q) {
-            int64_t c;
+        for (int q = 0; q < njobs; ++q) {
+            int c, t0, t1;
             bool is_scan;
             mc_job(q, gm.chunks, p.ahead, c, is_scan);
-            int64_t lo, hi;
-            block_range(c, lo, hi);
+            block_tiles(c, t0, t1);
             if (!is_scan) {
                 // ---------------- Phase I: block reduction r[c][b] ----------------
                 Carry jsum = Carry(0);
-                for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++q_tile) {
-                    const int s = (int)(q_tile % NB_IN);
-                    mbar_wait_prof(&in_full[s], (uint32_t)(q_tile / NB_IN) & 1u, prof && cw == 0 && lane == 0,
-                                   &s_prof[1]);
-                    const long long tr0 = clock64();
-                    const int m = (int)(hi - g0 < TILE ? hi - g0 : TILE);
-                    int64_t mt = p.n_tma_in - g0;
-                    const int m_tma = (int)(mt < 0 ? 0 : (mt > m ? m : mt));
-                    const uint8_t* slot = in_ring + s * Cfg::kRingSlot;
+                for (int t = t0; t < t1; ++t, rin.next()) {
+                    mbar_wait_prof(&in_full[rin.s], rin.ph, prof0, &s_prof[1]);
+                    const long long tr0 = prof ? clock64() : 0;
+                    const uint8_t* slot = in_ring + rin.s * Cfg::kRingSlot;
+                    if (t < gm.full_tiles) {
 #pragma unroll
-                    for (int g = 0; g < GPW; ++g) {
-                        const int e0 = (cw * GPW + g) * 512 + 16 * lane;
-                        Acc v[16];
-                        load_lane(slot, g0, e0, m, m_tma, v);
-                        // pairwise within the lane (fp32), then fp64 across tiles
-                        Acc s8[8];
+                        for (int g = 0; g < GPW; ++g) {
+                            Grp<SZ> gr;
+                            grp_load_off(slot + g * GI, off.in, gr);
+                            jsum = jsum + Carry(grp_sum(gr, (const In*)nullptr));
+                        }
+                    } else {
+                        int m, m_in, m_out;
+                        ragged(t, m, m_in, m_out);
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) s8[k] = v[2 * k] + v[2 * k + 1];
-                        const Acc s4a = (s8[0] + s8[1]) + (s8[2] + s8[3]);
-                        const Acc s4b = (s8[4] + s8[5]) + (s8[6] + s8[7]);
-                        jsum = jsum + Carry(s4a + s4b);
+                        for (int g = 0; g < GPW; ++g) {
+                            Grp<SZ> gr;
+                            grp_load_tail(slot, gin_b + (int64_t)t * TILE * SZ, e0_base + 512 * g, m, m_in, gr);
+                            jsum = jsum + Carry(grp_sum(gr, (const In*)nullptr));
+                        }
                     }
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(&in_empty[s]);
-                    if (prof && cw == 0 && lane == 0) {
+                    if (lane == 0) ptx::mbar_arrive(&in_empty[rin.s]);
+                    if (prof0) {
                         s_prof[8] += 1;
                         s_prof[10] += (unsigned long long)(clock64() - tr0);
                     }
@@ -538,29 +744,29 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 }
             } else {
                 // ---------------- Phase II: scan with the block carry ----------------
-                mbar_wait_prof(&carry_ready[c % KC], (uint32_t)(c / KC) & 1u, prof && cw == 0 && lane == 0,
-                               &s_prof[0]);
+                mbar_wait_prof(&carry_ready[c % KC], (uint32_t)(c / KC) & 1u, prof0, &s_prof[0]);
                 Carry carry = s_carry[c % KC];
-                for (int64_t g0 = lo; g0 < hi; g0 += TILE, ++q_tile, ++o_tile, ++s_count) {
-                    const int s = (int)(q_tile % NB_IN);
-                    const int o = UNI ? s : (int)(o_tile % NB_OUT);
-                    mbar_wait_prof(&in_full[s], (uint32_t)(q_tile / NB_IN) & 1u, prof && cw == 0 && lane == 0,
-                                   &s_prof[2]);
-                    const long long ts0 = clock64();
-                    const int m = (int)(hi - g0 < TILE ? hi - g0 : TILE);
-                    int64_t mt = p.n_tma_in - g0;
-                    const int m_tma = (int)(mt < 0 ? 0 : (mt > m ? m : mt));
+                for (int t = t0; t < t1; ++t, rin.next(), rout.next(), ++s_count) {
+                    const int s = rin.s;
+                    const int o = UNI ? s : rout.s;
+                    mbar_wait_prof(&in_full[s], rin.ph, prof0, &s_prof[2]);
+                    const long long ts0 = prof ? clock64() : 0;
+                    const bool full = t < gm.full_tiles;  // warp-uniform
+                    int m = TILE, m_in = TILE, m_out = TILE;
+                    if (!full) ragged(t, m, m_in, m_out);
                     const uint8_t* slot = in_ring + s * Cfg::kRingSlot;
 
-                    Acc v[GPW][16];
+                    LaneScan<DT> ls[GPW];
                     Acc ex[GPW], gp[GPW];
                     Acc wsum = Acc(0);
 #pragma unroll
                     for (int g = 0; g < GPW; ++g) {
-                        const int e0 = (cw * GPW + g) * 512 + 16 * lane;
-                        load_lane(slot, g0, e0, m, m_tma, v[g]);
-#pragma unroll
-                        for (int k = 1; k < 16; ++k) v[g][k] = v[g][k - 1] + v[g][k];
+                        if (full)
+                            grp_load_off(slot + g * GI, off.in, ls[g].g);
+                        else
+                            grp_load_tail(slot, gin_b + (int64_t)t * TILE * SZ, e0_base + 512 * g, m, m_in,
+                                          ls[g].g);
+                        ex[g] = ls[g].prefix();  // lane total (held in ex until the shuffle scan)
                     }
                     if (!UNI) {  // unified ring: the storer frees the slot after the store
                         __syncwarp();
@@ -568,77 +774,62 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     }
 #pragma unroll
                     for (int g = 0; g < GPW; ++g) {
-                        const Acc incl = warp_incl_scan(v[g][15], lane);
+                        const Acc incl = warp_incl_scan(ex[g], lane);
                         const Acc e1 = __shfl_up_sync(0xffffffffu, incl, 1);
                         ex[g] = lane == 0 ? Acc(0) : e1;
                         gp[g] = wsum;
                         wsum = wsum + __shfl_sync(0xffffffffu, incl, 31);
                     }
                     if (lane == 0) s_wt[s_count & 1][cw] = wsum;
-                    const long long ts1 = clock64();
+                    const long long ts1 = prof ? clock64() : 0;
                     named_bar_sync(1, NC * 32);
-                    const long long ts2 = clock64();
+                    const long long ts2 = prof ? clock64() : 0;
                     const Acc x = lane < NC ? s_wt[s_count & 1][lane] : Acc(0);
                     const Acc xi = warp_incl_scan(x, lane);
                     const Acc xe = __shfl_up_sync(0xffffffffu, xi, 1);
                     const Acc wpref = __shfl_sync(0xffffffffu, lane == 0 ? Acc(0) : xe, cw);
                     const Acc agg = __shfl_sync(0xffffffffu, xi, NC - 1);
-                    const long long te0 = clock64();
-                    if (!UNI && o_tile >= NB_OUT)
-                        mbar_wait_prof(&out_empty[o], (uint32_t)(o_tile / NB_OUT - 1) & 1u,
-                                       prof && cw == 0 && lane == 0, &s_prof[3]);
+                    const long long te0 = prof ? clock64() : 0;
+                    if (!UNI && rout.wrapped) mbar_wait_prof(&out_empty[o], rout.ph ^ 1u, prof0, &s_prof[3]);
                     uint8_t* ost = out_ring + o * Cfg::kOutSlot;
-                    const long long te1 = clock64();
+                    const long long te1 = prof ? clock64() : 0;
 #pragma unroll
                     for (int g = 0; g < GPW; ++g) {
-                        const int e0 = (cw * GPW + g) * 512 + 16 * lane;
                         Acc B;
                         if constexpr (Tr::kFloat)
                             B = (float)(carry + (double)((wpref + gp[g]) + ex[g]));
                         else
                             B = carry + wpref + gp[g] + ex[g];
                         Acc o16[16];
-                        if (p.exclusive) {
-                            o16[0] = B;
-#pragma unroll
-                            for (int k = 1; k < 16; ++k) o16[k] = B + v[g][k - 1];
+                        ls[g].emit(B, exclusive, o16);
+                        if (full) {
+                            store16_off(ost + g * GO, off.out, o16);
                         } else {
-#pragma unroll
-                            for (int k = 0; k < 16; ++k) o16[k] = B + v[g][k];
-                        }
-                        if (g0 + e0 + 16 <= p.n_tma_out) {
-                            store16(ost, e0, o16);
-                        } else {
+                            const int e0 = e0_base + 512 * g;
 #pragma unroll
                             for (int k = 0; k < 16; ++k) {
-                                const int64_t gi = g0 + e0 + k;
-                                if (gi < p.n_tma_out)
+                                if (e0 + k < m_out)
                                     *reinterpret_cast<Acc*>(ost + swz_elem<4>(e0 + k)) = o16[k];
                                 else if (e0 + k < m)
-                                    gout[gi] = narrow(o16[k], (Out*)nullptr);
+                                    gout[(int64_t)t * TILE + e0 + k] = narrow(o16[k], (Out*)nullptr);
                             }
                         }
                     }
-                    const long long te2 = clock64();
+                    const long long te2 = prof ? clock64() : 0;
                     ptx::fence_proxy_async_smem();
                     __syncwarp();
-                    const long long te3 = clock64();
-                    if (prof && cw == 0 && lane == 0) {
+                    if (lane == 0) ptx::mbar_arrive(&store_ready[o]);
+                    carry = carry + Carry(agg);
+                    if (prof0) {
+                        const long long te3 = clock64();
                         s_prof[14] += (unsigned long long)(te0 - ts2);
                         s_prof[15] += (unsigned long long)(te1 - te0);
                         s_prof[16] += (unsigned long long)(te2 - te1);
                         s_prof[17] += (unsigned long long)(te3 - te2);
-                    }
-                    if (lane == 0) {
-                        if (cw == 0) s_store_g0[o] = g0;
-                        ptx::mbar_arrive(&store_ready[o]);
-                    }
-                    carry = carry + Carry(agg);
-                    if (prof && cw == 0 && lane == 0) {
                         s_prof[9] += 1;
                         s_prof[11] += (unsigned long long)(ts1 - ts0);
                         s_prof[12] += (unsigned long long)(ts2 - ts1);
-                        s_prof[13] += (unsigned long long)(clock64() - ts2);
+                        s_prof[13] += (unsigned long long)(te3 - ts2);
                     }
                 }
             }
@@ -655,7 +846,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         const uint32_t prev = atomicAdd(&hdr->done, 1u);
         if (prev == gridDim.x - 1) {
             // every CTA is past every barrier: reset the counters for the next call
-            for (int64_t c = 0; c < gm.chunks; ++c) bar[c] = 0;
+            for (int c = 0; c < gm.chunks; ++c) bar[c] = 0;
             hdr->done = 0;
             __threadfence();
         }

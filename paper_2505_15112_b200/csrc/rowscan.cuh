@@ -196,26 +196,22 @@ __global__ void __launch_bounds__((2 + NC) * 32, 1) k_rowscan16(const __grid_con
             const int m = (int)(p.cols - (int64_t)k * TILE < TILE ? p.cols - (int64_t)k * TILE : TILE);
             uint8_t* const slot = ring + s * Cfg::kSlot;
 
-            Acc v[GPW][16];
+            LaneScan<DT> ls[GPW];
             Acc ex[GPW], gp[GPW];
             Acc wsum = Acc(0);
+            const bool full = m == TILE;  // warp-uniform
 #pragma unroll
             for (int g = 0; g < GPW; ++g) {
                 const int e0 = (cw * GPW + g) * 512 + 16 * lane;
-                if (e0 + 16 <= m) {
-                    load16(slot, e0, v[g], (const In*)nullptr);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j)
-                        v[g][j] = e0 + j < m ? widen(*reinterpret_cast<const In*>(slot + swz_elem<sizeof(In)>(e0 + j)))
-                                             : Acc(0);
-                }
-#pragma unroll
-                for (int j = 1; j < 16; ++j) v[g][j] = v[g][j - 1] + v[g][j];
+                if (full || e0 + 16 <= m)
+                    grp_load(slot, e0, ls[g].g);
+                else
+                    grp_load_tail(slot, slot, e0, m, m, ls[g].g);
+                ex[g] = ls[g].prefix();  // lane total until the shuffle scan
             }
 #pragma unroll
             for (int g = 0; g < GPW; ++g) {
-                const Acc incl = warp_incl_scan(v[g][15], lane);
+                const Acc incl = warp_incl_scan(ex[g], lane);
                 const Acc e1 = __shfl_up_sync(0xffffffffu, incl, 1);
                 ex[g] = lane == 0 ? Acc(0) : e1;
                 gp[g] = wsum;
@@ -228,6 +224,7 @@ __global__ void __launch_bounds__((2 + NC) * 32, 1) k_rowscan16(const __grid_con
             const Acc xe = __shfl_up_sync(0xffffffffu, xi, 1);
             const Acc wpref = __shfl_sync(0xffffffffu, lane == 0 ? Acc(0) : xe, cw);
             const Acc agg = __shfl_sync(0xffffffffu, xi, NC - 1);
+            const bool exclusive = p.exclusive != 0;
 #pragma unroll
             for (int g = 0; g < GPW; ++g) {
                 const int e0 = (cw * GPW + g) * 512 + 16 * lane;
@@ -237,14 +234,7 @@ __global__ void __launch_bounds__((2 + NC) * 32, 1) k_rowscan16(const __grid_con
                 else
                     B = carry + wpref + gp[g] + ex[g];
                 Acc o16[16];
-                if (p.exclusive) {
-                    o16[0] = B;
-#pragma unroll
-                    for (int j = 1; j < 16; ++j) o16[j] = B + v[g][j - 1];
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) o16[j] = B + v[g][j];
-                }
+                ls[g].emit(B, exclusive, o16);
                 store16(slot, e0, o16);  // columns past `cols` fall outside the tensor: not stored
             }
             ptx::fence_proxy_async_smem();

@@ -229,9 +229,10 @@ struct Mc16Variant {
     using Cfg = Mc16Cfg<DT, NC, GPW, NBI, NBO>;
     static constexpr int kTile = Cfg::kTile;
 
-    static int launch(const ScanParams& sp, cudaStream_t s, const DevInfo& di, int bt)
+    static int launch(const ScanParams& sp, cudaStream_t s, const DevInfo& di, int bt, int ahead)
     {
         using In = typename Traits<DT>::In;
+        if constexpr (Cfg::kSmem > 232448) return SCAN_ERR_ARG;  // tuning variant does not fit this dtype
         static std::once_flag once;
         static cudaError_t err = cudaSuccess;
         std::call_once(once, [] {
@@ -258,21 +259,21 @@ struct Mc16Variant {
         p.ws = sp.ws;
         p.exclusive = sp.exclusive;
         p.debug = debug_bits();
-        p.ahead = env_int("SCAN_MC_AHEAD", 1);
+        p.ahead = ahead < 1 ? 1 : (ahead > 2 ? 2 : ahead);
         p.gm.n = n;
-        p.gm.tile = kTile;
         p.gm.g = di.sms < kMaxGrid ? di.sms : kMaxGrid;
-        const int64_t per_cta = (n + (int64_t)p.gm.g * kTile - 1) / ((int64_t)p.gm.g * kTile);
-        p.gm.bt = bt < per_cta ? bt : (per_cta < 1 ? 1 : per_cta);
-        p.gm.block = p.gm.bt * kTile;
-        p.gm.chunk = p.gm.block * p.gm.g;
-        p.gm.chunks = (n + p.gm.chunk - 1) / p.gm.chunk;
-        if (p.gm.chunks > kMaxChunks) {  // larger blocks so the counters fit
-            p.gm.bt = (n + (int64_t)kMaxChunks * p.gm.g * kTile - 1) / ((int64_t)kMaxChunks * p.gm.g * kTile);
-            p.gm.block = p.gm.bt * kTile;
-            p.gm.chunk = p.gm.block * p.gm.g;
-            p.gm.chunks = (n + p.gm.chunk - 1) / p.gm.chunk;
-        }
+        const int64_t ntiles = (n + kTile - 1) / kTile;
+        int64_t lim = n < p.n_tma_in ? n : p.n_tma_in;
+        lim = lim < p.n_tma_out ? lim : p.n_tma_out;
+        p.gm.ntiles = (int)ntiles;
+        p.gm.full_tiles = (int)(lim / kTile);
+        const int64_t per_cta = (ntiles + p.gm.g - 1) / p.gm.g;
+        int64_t bt64 = bt < per_cta ? bt : (per_cta < 1 ? 1 : per_cta);
+        if ((ntiles + (int64_t)p.gm.g * bt64 - 1) / ((int64_t)p.gm.g * bt64) > kMaxChunks)  // counters must fit
+            bt64 = (ntiles + (int64_t)kMaxChunks * p.gm.g - 1) / ((int64_t)kMaxChunks * p.gm.g);
+        p.gm.bt = (int)bt64;
+        p.gm.chunk_tiles = p.gm.g * p.gm.bt;
+        p.gm.chunks = (int)((ntiles + p.gm.chunk_tiles - 1) / p.gm.chunk_tiles);
         void* args[] = {&p};
         cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_mcscan16<DT, NC, GPW, NBI, NBO>,
                                                     dim3(p.gm.g), dim3(Cfg::kThreads), args, Cfg::kSmem, s);
@@ -289,48 +290,42 @@ size_t mc_workspace_bytes(int64_t n)
     return kWsDescOffset + (size_t)blocks * 8 + 64;
 }
 
-// Chunk = G blocks of bt tiles; ~16 MB of input per chunk keeps two chunks'
-// inputs resident in the 126 MB L2 next to the streaming outputs.
+// Chunk = G blocks of bt tiles.  Reductions run `ahead` chunks ahead of the
+// scans, so (ahead + 1) chunks of input must stay resident in L2 between
+// their HBM read (Phase I) and their re-read (Phase II).  Measured on B200
+// (DESIGN.md section 8): the re-read stays in L2 while that footprint is about
+// 32 MB (126 MB L2 split over two dies, output streaming through it), and
+// bt >= 2 tiles per block keeps the per-chunk coordination (grid barrier,
+// 148 block sums per CTA) off the critical path; ahead = 2 absorbs barrier skew.
 template <typename V, int DT>
 int launch_mc_sized(const ScanParams& p, cudaStream_t s, const DevInfo& di)
 {
     using In = typename Traits<DT>::In;
     const int64_t tile_bytes = (int64_t)V::kTile * (int64_t)sizeof(In);
-    const int64_t want = (int64_t)env_int("SCAN_MC_CHUNK_MB", 16) << 20;
-    int64_t bt = (want + di.sms * tile_bytes / 2) / (di.sms * tile_bytes);
-    bt = bt < 1 ? 1 : bt;
-    return V::launch(p, s, di, env_int("SCAN_MC_BT", (int)bt));
+    const int ahead = env_int("SCAN_MC_AHEAD", 2);
+    const int64_t resident = (int64_t)env_int("SCAN_MC_RESIDENT_MB", 32) << 20;
+    const int64_t per_bt = (int64_t)(ahead + 1) * di.sms * tile_bytes;
+    int64_t bt = (resident + per_bt / 2) / per_bt;
+    bt = bt < 2 ? 2 : bt;
+    return V::launch(p, s, di, env_int("SCAN_MC_BT", (int)bt), ahead);
 }
 
+// Default variant per dtype (warps, groups per warp, input slots, output slots;
+// 0 output slots = outputs in place in the input ring); SCAN_MC selects
+// alternatives for tuning runs.
 template <int DT>
 int launch_mc(const ScanParams& p, cudaStream_t s, const DevInfo& di)
 {
     constexpr bool wide_in = (DT == SCAN_I32_I32 || DT == SCAN_F32_F32);
     switch (env_int("SCAN_MC", 0)) {
-    case 0:
+    case 1:
         if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 2, 2, 1>, DT>(p, s, di);
-        else if constexpr (DT == SCAN_F16_F32) return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 2>, DT>(p, s, di);
         else return launch_mc_sized<Mc16Variant<DT, 16, 2, 4, 2>, DT>(p, s, di);
-    case 4:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 1, 3, 3>, DT>(p, s, di);
-        else return launch_mc_sized<Mc16Variant<DT, 16, 1, 4, 3>, DT>(p, s, di);
-    case 5:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 12, 2, 2, 2>, DT>(p, s, di);
-        else return launch_mc_sized<Mc16Variant<DT, 12, 2, 3, 2>, DT>(p, s, di);
-    case 6:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 24, 1, 2, 2>, DT>(p, s, di);
-        else return launch_mc_sized<Mc16Variant<DT, 24, 1, 3, 2>, DT>(p, s, di);
     case 7: return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 0>, DT>(p, s, di);   // unified in-place ring
-    case 8:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 12, 2, 3, 1>, DT>(p, s, di);
-        else return launch_mc_sized<Mc16Variant<DT, 16, 2, 6, 2>, DT>(p, s, di);
-    case 9:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 24, 1, 3, 1>, DT>(p, s, di);
-        else return launch_mc_sized<Mc16Variant<DT, 12, 2, 4, 2>, DT>(p, s, di);
     default:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 2, 2, 1>, DT>(p, s, di);
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 12, 2, 3, 1>, DT>(p, s, di);
         else if constexpr (DT == SCAN_F16_F32) return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 2>, DT>(p, s, di);
-        else return launch_mc_sized<Mc16Variant<DT, 16, 2, 4, 2>, DT>(p, s, di);
+        else return launch_mc_sized<Mc16Variant<DT, 16, 2, 6, 2>, DT>(p, s, di);
     }
 }
 
