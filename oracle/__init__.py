@@ -53,9 +53,9 @@ def build() -> str:
 def lib():
     global _lib
     if _lib is None:
-        src = os.path.join(_HERE, "oracle_scan.c")
+        srcs = [os.path.join(_HERE, f) for f in ("oracle_scan.c", "oracle_ops.c")]
         if (not os.path.exists(_LIB_PATH)
-                or os.path.getmtime(_LIB_PATH) < os.path.getmtime(src)):
+                or os.path.getmtime(_LIB_PATH) < max(os.path.getmtime(f) for f in srcs)):
             build()
         L = ctypes.CDLL(_LIB_PATH)
         P, I64, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
@@ -79,6 +79,17 @@ def lib():
         L.oracle_check_f32.restype = I64
         L.oracle_rows_f32.argtypes = [P, I64, I64, I64, I64, I, P, P, P]
         L.oracle_rows_i32.argtypes = [P, I64, I64, I64, I64, I, P]
+        # oracle_ops.c: scan applications (Sec. 5, App. B.3)
+        L.oracle_split.argtypes = [P, P, I64, I, I, P, P]
+        L.oracle_split.restype = I64
+        L.oracle_sort_encode.argtypes = [ctypes.c_uint32, I]
+        L.oracle_sort_encode.restype = ctypes.c_uint32
+        L.oracle_radix_sort.argtypes = [P, I64, I, I, P, P]
+        L.oracle_weighted_sample.argtypes = [P, I64, ctypes.c_double]
+        L.oracle_weighted_sample.restype = I64
+        L.oracle_top_p_sample.argtypes = [P, I64, ctypes.c_double, ctypes.c_double,
+                                          ctypes.POINTER(ctypes.c_int64)]
+        L.oracle_top_p_sample.restype = I64
         _lib = L
     return _lib
 
@@ -207,3 +218,60 @@ def check_f32(got, ref64, abs_w, rel=1e-6, abs_tol=1e-6):
     bad = lib().oracle_check_f32(_ptr(got), _ptr(ref64), _ptr(abs_w), got.shape[0], rel,
                                  abs_tol, ctypes.byref(worst), ctypes.byref(at))
     return int(bad), float(worst.value), int(at.value)
+
+
+# ---------------------------------------------------------------------------
+# Scan applications (oracle_ops.c): PAPER.md Sec. 5.1-5.5 and App. B.3.
+# ---------------------------------------------------------------------------
+KEY_TYPES = {"u16": 0, "i16": 1, "f16": 2, "u32": 3, "i32": 4, "f32": 5}
+_KEY_NP = {"u16": np.uint16, "i16": np.int16, "f16": np.float16, "u32": np.uint32,
+           "i32": np.int32, "f32": np.float32}
+
+
+def split(x, flags, compress: bool = False, with_idx: bool = True):
+    """P281-285 SplitInd / Compress: stable split, flag-true items first (R12).
+
+    Returns (z, idx, T): z has n items (split) or T items (compress)."""
+    x = np.ascontiguousarray(x)
+    f = np.ascontiguousarray(flags).view(np.int8) if np.asarray(flags).dtype != np.int8 \
+        else np.ascontiguousarray(flags)
+    n = x.shape[0]
+    assert f.shape[0] == n
+    z = np.empty_like(x)
+    idx = np.empty(n, np.int32) if with_idx else None
+    T = lib().oracle_split(_ptr(x), _ptr(f), n, x.dtype.itemsize, int(compress), _ptr(z),
+                           _ptr(idx))
+    if compress:
+        return z[:T], (idx[:T] if with_idx else None), int(T)
+    return z, idx, int(T)
+
+
+def sort_encode(bits: int, key_type: str) -> int:
+    """P287 float pre-processing (R13 for integers): order-preserving unsigned code."""
+    return int(lib().oracle_sort_encode(int(bits) & 0xFFFFFFFF, KEY_TYPES[key_type]))
+
+
+def radix_sort(keys, key_type: str, descending: bool = False):
+    """P286-287 LSB radix sort by one split per bit (R13).  Returns (sorted keys, idx)."""
+    k = np.ascontiguousarray(keys, dtype=_KEY_NP[key_type])
+    out = np.empty_like(k)
+    idx = np.empty(k.shape[0], np.int32)
+    lib().oracle_radix_sort(_ptr(k), k.shape[0], KEY_TYPES[key_type], int(descending), _ptr(out),
+                            _ptr(idx))
+    return out, idx
+
+
+def weighted_sample(w, theta: float) -> int:
+    """P463 inverse transform sampling on the scan of w (R14)."""
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    return int(lib().oracle_weighted_sample(_ptr(w), w.shape[0], float(theta)))
+
+
+def top_p_sample(probs, p: float, u: float):
+    """P298-299 top-p (nucleus) sampling: sort, scan, nucleus, sample (R15).
+
+    Returns (token index, nucleus size)."""
+    q = np.ascontiguousarray(probs, dtype=np.float32)
+    kept = ctypes.c_int64()
+    tok = lib().oracle_top_p_sample(_ptr(q), q.shape[0], float(p), float(u), ctypes.byref(kept))
+    return int(tok), int(kept.value)
