@@ -13,6 +13,8 @@ Public API (names follow the C ABI):
     total(x)                                  -- RSS reduction (P73)
     carry_from_totals(totals, rank)           -- sum of lower shard totals
     sharded_inclusive / sharded_exclusive     -- see paper_2505_15112_b200.dist
+    split(x, flags) / compress(x, flags)      -- P281-285 SplitInd / compress
+    radix_sort(keys, descending=False)        -- P286-287 LSB radix sort by splits
 """
 from __future__ import annotations
 
@@ -81,6 +83,15 @@ def load() -> ctypes.CDLL:
         L.scan_host_stage_bytes.restype = SZ
         L.scan_host.argtypes = [P, P, I64, I, I, I64, P, SZ, P, SZ, P]
         L.scan_host.restype = I
+        # include/scan_ops.h
+        L.scan_split_workspace_bytes.argtypes = [I64]
+        L.scan_split_workspace_bytes.restype = SZ
+        L.scan_split.argtypes = [P, P, P, P, I64, I, I, P, P, SZ, P]
+        L.scan_split.restype = I
+        L.scan_radix_sort_workspace_bytes.argtypes = [I64, I]
+        L.scan_radix_sort_workspace_bytes.restype = SZ
+        L.scan_radix_sort.argtypes = [P, P, P, I64, I, I, P, SZ, P]
+        L.scan_radix_sort.restype = I
         _lib = L
     return _lib
 
@@ -252,3 +263,68 @@ def host_scan(h_in: torch.Tensor, h_out=None, exclusive: bool = False, chunk: in
 
 def launch_count() -> int:
     return int(load().scan_launch_count())
+
+
+# ---------------------------------------------------------------- operators
+# include/scan_ops.h: split / compress (P281-285) and the LSB radix sort (P287).
+SCAN_KEY = {torch.int16: 1, torch.float16: 2, torch.int32: 4, torch.float32: 5}
+if hasattr(torch, "uint16"):
+    SCAN_KEY[torch.uint16] = 0
+if hasattr(torch, "uint32"):
+    SCAN_KEY[torch.uint32] = 3
+
+
+def split(x: torch.Tensor, flags: torch.Tensor, compress: bool = False, with_idx: bool = True,
+          out=None, idx_out=None, stream=None):
+    """P281-283 SplitInd: stable split, flag-true items first (nonzero int8 = true).
+
+    Returns (z, idx, count) with count a 1-element int64 CUDA tensor (T, the
+    number of true flags).  With compress=True (P285, = masked_select) only
+    the first T entries of z / idx are meaningful; see compress()."""
+    if not (x.is_cuda and flags.is_cuda):
+        raise ScanError("split expects CUDA tensors (there is no CPU path)")
+    if flags.dtype != torch.int8:
+        raise ScanError("flags must be int8")
+    x = x.reshape(-1)
+    flags = flags.reshape(-1)
+    if not (x.is_contiguous() and flags.is_contiguous()) or flags.numel() != x.numel():
+        raise ScanError("x and flags must be contiguous 1-D tensors of the same length")
+    n = x.numel()
+    z = torch.empty_like(x) if out is None else out
+    idx = (torch.empty(n, dtype=torch.int32, device=x.device) if idx_out is None else idx_out) \
+        if with_idx else None
+    cnt = torch.empty(1, dtype=torch.int64, device=x.device)
+    L = load()
+    ws = workspace(L.scan_split_workspace_bytes(n), x.device, stream)
+    _check(L.scan_split(_ptr(x), _ptr(flags), _ptr(z), _ptr(idx), n, x.element_size(), int(bool(compress)),
+                        _ptr(cnt), ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)), "scan_split")
+    return z, idx, cnt
+
+
+def compress(x: torch.Tensor, flags: torch.Tensor, with_idx: bool = False, stream=None):
+    """P285 compress (= torch.masked_select): the flag-true items of x in order.
+    Synchronises once to size the result."""
+    z, idx, cnt = split(x, flags, compress=True, with_idx=with_idx, stream=stream)
+    T = int(cnt.item())
+    return (z[:T], idx[:T]) if with_idx else z[:T]
+
+
+def radix_sort(keys: torch.Tensor, descending: bool = False, out=None, idx_out=None, stream=None):
+    """P286-287 stable LSB radix sort by one split per key bit (16 for 16-bit
+    keys, 32 for 32-bit); floats ordered by the IEEE total order (R13).
+
+    Returns (sorted keys, int32 input positions)."""
+    if not keys.is_cuda:
+        raise ScanError("radix_sort expects a CUDA tensor (there is no CPU path)")
+    if keys.dtype not in SCAN_KEY:
+        raise ScanError(f"unsupported key dtype {keys.dtype}")
+    keys = keys.reshape(-1).contiguous()
+    n = keys.numel()
+    kout = torch.empty_like(keys) if out is None else out
+    idx = torch.empty(n, dtype=torch.int32, device=keys.device) if idx_out is None else idx_out
+    L = load()
+    kt = SCAN_KEY[keys.dtype]
+    ws = workspace(L.scan_radix_sort_workspace_bytes(n, kt), keys.device, stream)
+    _check(L.scan_radix_sort(_ptr(keys), _ptr(kout), _ptr(idx), n, kt, int(bool(descending)),
+                             ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)), "scan_radix_sort")
+    return kout, idx

@@ -1,0 +1,211 @@
+// ops_api.cuh -- C ABI of include/scan_ops.h (split / compress / radix sort),
+// compiled into scan_api.cu's translation unit so it shares its device cache
+// and launch counter.  Host code only: argument checks and launches.
+#pragma once
+#include "../../include/scan_ops.h"
+#include "split.cuh"
+
+namespace {
+
+using scan::split::SplitParams;
+using scan::split::kThreads;
+using scan::split::kTile;
+
+constexpr size_t kSplitHdr = 128;              // split header inside the scan header block
+constexpr size_t kSplitArrays = kWsDescOffset;  // counts[ntiles] then offs[ntiles]
+
+int64_t split_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
+
+size_t split_ws_bytes(int64_t n) { return kSplitArrays + (size_t)split_tiles(n) * 8 + 64; }
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+bool overlap(const void* a, size_t na, const void* b, size_t nb)
+{
+    const uintptr_t x = (uintptr_t)a, y = (uintptr_t)b;
+    return x < y + nb && y < x + na;
+}
+
+template <int SRC, int ES, int KT, bool IDX_IN>
+int launch_split_t(SplitParams& p, cudaStream_t s, const DevInfo& di)
+{
+    using namespace scan::split;
+    const size_t smem = (size_t)kTile * (ES + 4);
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    static int occ = 1;
+    std::call_once(once, [smem] {
+        err = cudaFuncSetAttribute(k_split_scatter<SRC, ES, KT, IDX_IN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem);
+        if (err == cudaSuccess &&
+            (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_split_scatter<SRC, ES, KT, IDX_IN>, kThreads, smem) !=
+                 cudaSuccess ||
+             occ < 1))
+            occ = 1;
+    });
+    if (err != cudaSuccess) return SCAN_ERR_CUDA;
+    // count: a warp per tile, up to 4 CTAs per SM; scatter: every resident CTA slot
+    const int64_t want_count = ((int64_t)p.ntiles + kWarps - 1) / kWarps;
+    const int64_t g_count = (int64_t)di.sms * 4 < want_count ? (int64_t)di.sms * 4 : want_count;
+    const int64_t g_scat = (int64_t)di.sms * occ < p.ntiles ? (int64_t)di.sms * occ : p.ntiles;
+    k_split_count<SRC, ES, KT><<<(unsigned)g_count, kThreads, 0, s>>>(p);
+    k_split_scatter<SRC, ES, KT, IDX_IN><<<(unsigned)g_scat, kThreads, smem, s>>>(p);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+}
+
+// TMA-ring scatter (split.cuh k_split_scatter_tma): aligned buffers, ES <= 4.
+template <int SRC, int ES, int KT, bool IDX_IN>
+int launch_split_tma(SplitParams& p, cudaStream_t s, const DevInfo& di)
+{
+    using namespace scan::split;
+    using C = TmaCfg<SRC, ES, IDX_IN>;
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    std::call_once(once, [] {
+        err = cudaFuncSetAttribute(k_split_scatter_tma<SRC, ES, KT, IDX_IN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)C::kSmem);
+    });
+    if (err != cudaSuccess) return SCAN_ERR_CUDA;
+    const int64_t want_count = ((int64_t)p.ntiles + kWarps - 1) / kWarps;
+    const int64_t g_count = (int64_t)di.sms * 4 < want_count ? (int64_t)di.sms * 4 : want_count;
+    const int64_t g_scat = (int64_t)di.sms < p.ntiles ? (int64_t)di.sms : p.ntiles;
+    k_split_count<SRC, ES, KT><<<(unsigned)g_count, kThreads, 0, s>>>(p);
+    k_split_scatter_tma<SRC, ES, KT, IDX_IN><<<(unsigned)g_scat, C::kThreadsT, C::kSmem, s>>>(p);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+}
+
+template <int SRC, int ES, int KT>
+int launch_split(SplitParams& p, cudaStream_t s, const DevInfo& di)
+{
+    if constexpr (ES <= 4) {
+        if (p.aligned && getenv("SCAN_SPLIT_NO_TMA") == nullptr) {
+            if constexpr (SRC == scan::split::SRC_KEYBIT)
+                if (p.idx_in) return launch_split_tma<SRC, ES, KT, true>(p, s, di);
+            return launch_split_tma<SRC, ES, KT, false>(p, s, di);
+        }
+    }
+    return p.idx_in ? launch_split_t<SRC, ES, KT, true>(p, s, di) : launch_split_t<SRC, ES, KT, false>(p, s, di);
+}
+
+template <int KT>
+int launch_sort_pass(SplitParams& p, cudaStream_t s, const DevInfo& di)
+{
+    using namespace scan::split;
+    return launch_split<SRC_KEYBIT, (KT <= KEY_F16 ? 2 : 4), KT>(p, s, di);
+}
+
+void split_ws_setup(SplitParams& p, void* ws, int64_t n)
+{
+    uint8_t* w = (uint8_t*)ws;
+    p.hdr = reinterpret_cast<uint32_t*>(w + kSplitHdr);
+    p.counts = reinterpret_cast<uint32_t*>(w + kSplitArrays);
+    p.offs = p.counts + split_tiles(n);
+    p.n = n;
+    p.ntiles = (int)split_tiles(n);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t scan_split_workspace_bytes(int64_t n)
+{
+    if (n < 0) return 0;
+    return split_ws_bytes(n);
+}
+
+int scan_split(const void* x, const int8_t* flags, void* z, int32_t* idx_out, int64_t n, int elem_bytes,
+               int compress, int64_t* count_out, void* ws, size_t ws_bytes, void* stream)
+{
+    if (n < 0 || n >= ((int64_t)1 << 31)) return SCAN_ERR_ARG;
+    if (!(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8)) return SCAN_ERR_ARG;
+    if (ws == nullptr || ((uintptr_t)ws & 255u) != 0 || ws_bytes < split_ws_bytes(n)) return SCAN_ERR_WORKSPACE;
+    if (n > 0 && (x == nullptr || flags == nullptr || z == nullptr)) return SCAN_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n == 0) {
+        if (count_out && cudaMemsetAsync(count_out, 0, sizeof(int64_t), s) != cudaSuccess) return SCAN_ERR_CUDA;
+        return SCAN_OK;
+    }
+    if (overlap(x, (size_t)n * elem_bytes, z, (size_t)n * elem_bytes)) return SCAN_ERR_ARG;
+    DevInfo di;
+    int st = dev_info(di);
+    if (st != SCAN_OK) return st;
+    SplitParams p;
+    memset(&p, 0, sizeof(p));
+    split_ws_setup(p, ws, n);
+    p.x = x;
+    p.z = z;
+    p.flags = flags;
+    p.idx_out = idx_out;
+    p.count_out = count_out;
+    p.compress = compress != 0;
+    p.aligned = aligned16(x) && aligned16(z) && aligned16(flags) && (idx_out == nullptr || aligned16(idx_out));
+    using namespace scan::split;
+    switch (elem_bytes) {
+    case 1: return launch_split<SRC_FLAGS, 1, 0>(p, s, di);
+    case 2: return launch_split<SRC_FLAGS, 2, 0>(p, s, di);
+    case 4: return launch_split<SRC_FLAGS, 4, 0>(p, s, di);
+    default: return launch_split<SRC_FLAGS, 8, 0>(p, s, di);
+    }
+}
+
+size_t scan_radix_sort_workspace_bytes(int64_t n, int key_type)
+{
+    if (n < 0 || key_type < SCAN_KEY_U16 || key_type > SCAN_KEY_F32) return 0;
+    const size_t es = key_type <= SCAN_KEY_F16 ? 2 : 4;
+    auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    return up(split_ws_bytes(n)) + up((size_t)n * es) + up((size_t)n * 4);
+}
+
+int scan_radix_sort(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, int key_type, int descending,
+                    void* ws, size_t ws_bytes, void* stream)
+{
+    if (n < 0 || n >= ((int64_t)1 << 31) || key_type < SCAN_KEY_U16 || key_type > SCAN_KEY_F32) return SCAN_ERR_ARG;
+    const size_t need = scan_radix_sort_workspace_bytes(n, key_type);
+    if (ws == nullptr || ((uintptr_t)ws & 255u) != 0 || ws_bytes < need) return SCAN_ERR_WORKSPACE;
+    if (n > 0 && (keys == nullptr || keys_out == nullptr || idx_out == nullptr)) return SCAN_ERR_ARG;
+    if (n == 0) return SCAN_OK;
+    const int es = key_type <= SCAN_KEY_F16 ? 2 : 4;
+    if (overlap(keys, (size_t)n * es, keys_out, (size_t)n * es)) return SCAN_ERR_ARG;
+    DevInfo di;
+    int st = dev_info(di);
+    if (st != SCAN_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    uint8_t* w = (uint8_t*)ws;
+    void* tmp_keys = w + up(split_ws_bytes(n));
+    int32_t* tmp_idx = reinterpret_cast<int32_t*>(w + up(split_ws_bytes(n)) + up((size_t)n * es));
+    const int bits = es * 8;  // even: pass 0 writes tmp, the last pass writes keys_out
+    SplitParams p;
+    memset(&p, 0, sizeof(p));
+    split_ws_setup(p, ws, n);
+    p.descending = descending != 0;
+    const void* src_k = keys;
+    const int32_t* src_i = nullptr;  // pass 0: indices are the positions
+    for (int b = 0; b < bits; ++b) {
+        void* dk = (b & 1) ? keys_out : tmp_keys;
+        int32_t* di_ = (b & 1) ? idx_out : tmp_idx;
+        p.x = src_k;
+        p.z = dk;
+        p.idx_in = src_i;
+        p.idx_out = di_;
+        p.bit = b;
+        p.aligned = aligned16(src_k) && aligned16(dk) && aligned16(di_) && (src_i == nullptr || aligned16(src_i));
+        switch (key_type) {
+        case SCAN_KEY_U16: st = launch_sort_pass<scan::split::KEY_U16>(p, s, di); break;
+        case SCAN_KEY_I16: st = launch_sort_pass<scan::split::KEY_I16>(p, s, di); break;
+        case SCAN_KEY_F16: st = launch_sort_pass<scan::split::KEY_F16>(p, s, di); break;
+        case SCAN_KEY_U32: st = launch_sort_pass<scan::split::KEY_U32>(p, s, di); break;
+        case SCAN_KEY_I32: st = launch_sort_pass<scan::split::KEY_I32>(p, s, di); break;
+        default: st = launch_sort_pass<scan::split::KEY_F32>(p, s, di); break;
+        }
+        if (st != SCAN_OK) return st;
+        src_k = dk;
+        src_i = di_;
+    }
+    return SCAN_OK;
+}
+
+}  // extern "C"

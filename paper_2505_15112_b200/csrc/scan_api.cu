@@ -752,3 +752,6 @@ int scan_host(const void* h_in, void* h_out, int64_t n, int dtype, int exclusive
 }
 
 }  // extern "C"
+
+// ---- scan-based operators (include/scan_ops.h) ----
+#include "ops_api.cuh"

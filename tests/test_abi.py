@@ -8,7 +8,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def declared_symbols():
-    src = open(os.path.join(ROOT, "include", "scan.h")).read()
+    src = "".join(open(os.path.join(ROOT, "include", h)).read() for h in ("scan.h", "scan_ops.h"))
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     return sorted(set(re.findall(r"\b(scan_[a-z_0-9]+)\s*\(", src)))
 
@@ -37,6 +37,13 @@ def test_library_exports_every_declared_symbol():
     # argument errors are reported before touching CUDA
     assert L.scan_inclusive(None, None, -5, 0, None, None, 0, None) == 1
     assert L.scan_inclusive(None, None, 0, 0, None, None, 0, None) == 0
+    # operators (include/scan_ops.h)
+    assert L.scan_split_workspace_bytes(-1) == 0
+    assert L.scan_split_workspace_bytes(1 << 20) > L.scan_split_workspace_bytes(0)
+    assert L.scan_radix_sort_workspace_bytes(10, 9) == 0
+    assert L.scan_split(None, None, None, None, -1, 2, 0, None, None, 0, None) == 1
+    assert L.scan_split(None, None, None, None, 10, 3, 0, None, None, 0, None) == 1
+    assert L.scan_radix_sort(None, None, None, 10, 7, 0, None, 0, None) == 1
 
 
 def test_product_has_no_oracle_or_cpu_path():

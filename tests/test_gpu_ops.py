@@ -1,0 +1,141 @@
+"""GPU parity of the scan-based operators (include/scan_ops.h) against the CPU
+oracle (oracle/oracle_ops.c): split / compress (P281-285) and the LSB radix
+sort by per-bit splits (P286-287).  All results are integer / byte moves, so
+every comparison is bit-exact.  Sizes span several 8192-element tiles and
+ragged tails; edge cases: empty, 1 element, unaligned buffers, all-true /
+all-false masks, nonzero flags other than 1 (R12), NaN / inf / signed zeros.
+At full size (the C3 mask, n = 2^30) the outputs are checked by properties
+that pin a split completely."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [1, 15, 16, 17, 8191, 8192, 8193, 3 * 8192 + 5, 100003, (1 << 20) + 3]
+PAYLOAD = {1: torch.int8, 2: torch.float16, 4: torch.int32, 8: torch.int64}
+
+
+def _flags(inputs_mod, n, seed):
+    return inputs_mod.fill_host(inputs_mod.I8_FLAG, seed, 0, n)
+
+
+def _payload(n, es, seed):
+    rng = np.random.default_rng(seed)
+    raw = rng.integers(0, 256, n * es, dtype=np.uint8)
+    return torch.from_numpy(raw).view(PAYLOAD[es]).cuda(), raw.view({1: np.int8, 2: np.uint16, 4: np.int32, 8: np.int64}[es])
+
+
+@pytest.mark.parametrize("es", [1, 2, 4, 8])
+@pytest.mark.parametrize("compress", [False, True])
+def test_split_sizes(cuda, oracle, inputs_mod, es, compress):
+    for n in SIZES:
+        f = _flags(inputs_mod, n, seed=n)
+        xd, xh = _payload(n, es, seed=n + es)
+        z, idx, cnt = cuda.split(xd, torch.from_numpy(f).cuda(), compress=compress)
+        zr, ir, T = oracle.split(xh, f, compress=compress)
+        assert int(cnt.item()) == T
+        m = T if compress else n
+        got = z[:m].cpu().numpy().view(xh.dtype)
+        assert np.array_equal(got, zr), (n, es)
+        assert np.array_equal(idx[:m].cpu().numpy(), ir), (n, es)
+
+
+def test_split_edge_cases(cuda, oracle):
+    dev = torch.device("cuda")
+    # empty
+    z, idx, cnt = cuda.split(torch.empty(0, dtype=torch.int32, device=dev), torch.empty(0, dtype=torch.int8, device=dev))
+    assert z.numel() == 0 and int(cnt.item()) == 0
+    n = 3 * 8192 + 7
+    x = np.arange(n, dtype=np.int32)
+    for f in (np.ones(n, np.int8), np.zeros(n, np.int8),
+              np.random.default_rng(1).choice(np.array([0, 1, -3, 2, 127, -128], np.int8), n)):
+        z, idx, cnt = cuda.split(torch.from_numpy(x).cuda(), torch.from_numpy(f).cuda())
+        zr, ir, T = oracle.split(x, f)
+        assert int(cnt.item()) == T
+        assert np.array_equal(z.cpu().numpy(), zr) and np.array_equal(idx.cpu().numpy(), ir)
+
+
+def test_split_unaligned(cuda, oracle, inputs_mod):
+    n = 50001
+    f = _flags(inputs_mod, n + 3, seed=7)
+    xd, xh = _payload(n + 3, 2, seed=8)
+    fd = torch.from_numpy(f).cuda()
+    for off in (1, 3):
+        z, idx, cnt = cuda.split(xd[off:off + n], fd[off:off + n])
+        zr, ir, T = oracle.split(xh[off:off + n].copy(), f[off:off + n].copy())
+        assert int(cnt.item()) == T
+        assert np.array_equal(z.cpu().numpy().view(np.uint16), zr) and np.array_equal(idx.cpu().numpy(), ir)
+
+
+def test_compress_matches_masked_select(cuda, inputs_mod):
+    n = 1 << 20
+    f = torch.from_numpy(_flags(inputs_mod, n, seed=2)).cuda()
+    x = torch.randn(n, device="cuda")
+    got = cuda.compress(x, f)
+    assert torch.equal(got, torch.masked_select(x, f != 0))
+
+
+@pytest.mark.slow
+def test_split_full_size_properties(cuda, inputs_mod):
+    """C3's mask (n = 2^30, Bernoulli(0.5), seed 2) with an int16 payload: the
+    count equals the popcount, idx is the stable partition (trues ascending,
+    then falses ascending) and z = x[idx] -- which determines the split."""
+    n = 1 << 30
+    f = torch.empty(n, dtype=torch.int8, device="cuda")
+    inputs_mod.fill_device(inputs_mod.I8_FLAG, 2, 0, n, 0, f)
+    x = torch.arange(n, device="cuda", dtype=torch.int32).to(torch.int16)
+    z, idx, cnt = cuda.split(x, f)
+    T = int(cnt.item())
+    assert T == int(f.sum(dtype=torch.int64).item())
+    assert abs(T - n // 2) < 6 * (n ** 0.5) / 2
+    idx64 = idx.to(torch.int64)
+    assert bool((f[idx64[:T]] != 0).all()) and bool((f[idx64[T:]] == 0).all())
+    assert bool((idx64[1:T] > idx64[:T - 1]).all()) and bool((idx64[T + 1:] > idx64[T:-1]).all())
+    assert torch.equal(z, x[idx64])
+
+
+# ----------------------------------------------------------------- radix sort
+KEY_NP = {torch.float16: (np.float16, "f16"), torch.int16: (np.int16, "i16"),
+          torch.int32: (np.int32, "i32"), torch.float32: (np.float32, "f32")}
+
+
+def _keys(dt, n, seed):
+    rng = np.random.default_rng(seed)
+    npdt, _ = KEY_NP[dt]
+    if dt in (torch.float16, torch.float32):
+        k = (rng.standard_normal(n) * 50).astype(npdt)
+        specials = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, -np.nan, 1.0, -1.0], npdt)
+        k[rng.integers(0, n, min(n, 64))] = rng.choice(specials, min(n, 64))
+    else:
+        info = np.iinfo(npdt)
+        k = rng.integers(info.min, info.max, n, endpoint=True).astype(npdt)
+    if n > 10:
+        k[::9] = k[5]  # ties: stability
+    return k
+
+
+@pytest.mark.parametrize("dt", [torch.float16, torch.int16, torch.int32, torch.float32])
+@pytest.mark.parametrize("desc", [False, True])
+def test_radix_sort_parity(cuda, oracle, dt, desc):
+    sizes = [1, 17, 8193, 100003] if dt in (torch.int32, torch.float32) else [1, 17, 8193, 100003, (1 << 18) + 9]
+    for n in sizes:
+        k = _keys(dt, n, seed=n)
+        kd = torch.from_numpy(k).cuda()
+        out, idx = cuda.radix_sort(kd, descending=desc)
+        ro, ri = oracle.radix_sort(k, KEY_NP[dt][1], descending=desc)
+        bits = np.uint16 if k.itemsize == 2 else np.uint32
+        assert np.array_equal(idx.cpu().numpy(), ri), (dt, n)
+        assert np.array_equal(out.cpu().numpy().view(bits), ro.view(bits)), (dt, n)
+
+
+def test_radix_sort_matches_torch_sort_stable(cuda):
+    """Against torch.sort(stable=True) (CUB) on NaN-free keys without -0."""
+    for dt in (torch.float16, torch.float32, torch.int32):
+        k = (torch.randn(1 << 20, device="cuda") * 1000).to(dt)
+        if dt.is_floating_point:
+            k[k == 0] = 1
+        for desc in (False, True):
+            out, idx = cuda.radix_sort(k, descending=desc)
+            ref, ridx = torch.sort(k, stable=True, descending=desc)
+            assert torch.equal(out, ref) and torch.equal(idx.to(torch.int64), ridx)
