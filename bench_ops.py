@@ -102,8 +102,31 @@ def main():
         alg = 16 * n * (2 + 2 + 4 + 4) - n * 4  # pass 0 reads no indices
         ref_fn = lambda: torch.sort(k, stable=True)  # noqa: E731
         ref_name = "torch.sort(stable=True) (CUB radix sort, int64 indices)"
-    else:
-        raise SystemExit(f"--op {args.op}: not built yet")
+    elif args.op == "weighted":
+        wgt = torch.empty(n, dtype=torch.float32, device=dev)
+        inputs.fill_device(inputs.F32_NORMAL, 6, 0, n, 0, wgt)
+        wgt = wgt.abs_()
+        cdf = torch.empty_like(wgt)
+        fn = lambda: S.weighted_sample(wgt, 0.37, cdf=cdf)  # noqa: E731
+        alg = n * 8  # the scan's in + out; the draw probes O(1) KB
+        ref_fn = lambda: torch.searchsorted(torch.cumsum(wgt, 0), 0.37 * wgt.sum(), right=True)  # noqa: E731
+        ref_name = "torch.cumsum + torch.searchsorted (torch.multinomial caps categories at 2^24)"
+    else:  # top_p
+        R, C = 4096, 131072
+        probs = torch.empty((R, C), dtype=torch.float32, device=dev)
+        inputs.fill_device(inputs.F32_SOFTMAX, 3, 0, R, C, probs)
+        uu = torch.rand(R, generator=torch.Generator(device=dev).manual_seed(7), device=dev)
+        fn = lambda: S.top_p_sample(probs, 0.9, uu)  # noqa: E731
+        alg = R * C * 4  # bytes of probabilities consumed per step
+
+        def ref_fn():
+            sp, order = torch.sort(probs, dim=1, descending=True, stable=True)
+            cs = torch.cumsum(sp, dim=1)
+            keep = (cs - sp) < 0.9
+            sp = sp * keep
+            tok = torch.searchsorted(torch.cumsum(sp, 1), (uu * sp.sum(1)).unsqueeze(1), right=True)
+            return order.gather(1, tok.clamp_max(C - 1))
+        ref_name = "torch.sort + torch.cumsum + mask + searchsorted (Llama-style top-p)"
 
     clocks = ClockSampler(0)
     clocks.start()
@@ -117,7 +140,26 @@ def main():
     # cpu_baseline: the oracle as it stands on a bounded sample of the same workload
     import oracle
     cn = 1 << 22 if args.op != "sort" else 1 << 18
-    if args.op in ("split", "compress"):
+    if args.op == "top_p":
+        cn = 131072
+        Ph = inputs.fill_host(inputs.F32_SOFTMAX, 3, 0, 1, C)[0]
+        t0 = time.perf_counter()
+        reps = 0
+        while time.perf_counter() - t0 < args.cpu_seconds:
+            oracle.top_p_sample(Ph, 0.9, 0.5)
+            reps += 1
+        ct = time.perf_counter() - t0
+        cpu_alg = cn * 4 * reps
+    elif args.op == "weighted":
+        wh = np.abs(inputs.fill_host(inputs.F32_NORMAL, 6, 0, cn))
+        t0 = time.perf_counter()
+        reps = 0
+        while time.perf_counter() - t0 < args.cpu_seconds:
+            oracle.weighted_sample(wh, 0.37)
+            reps += 1
+        ct = time.perf_counter() - t0
+        cpu_alg = cn * 8 * reps
+    elif args.op in ("split", "compress"):
         fh = inputs.fill_host(inputs.I8_FLAG, 2, 0, cn)
         xh = inputs.fill_host(inputs.F16_U01, 1, 0, cn)
         t0 = time.perf_counter()
@@ -140,7 +182,9 @@ def main():
         "metric": f"{args.op} GB/s (algorithmic bytes)", "value": round(value, 1), "unit": "GB/s",
         "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(med * 1e3, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp16 payload / int8 mask / int32 indices" if args.op != "sort" else "fp16 keys / int32 indices",
+        "dtype": {"split": "fp16 payload / int8 mask / int32 indices", "compress": "fp16 payload / int8 mask",
+                  "sort": "fp16 keys / int32 indices", "weighted": "f32 (fp64 carry)",
+                  "top_p": "f32 probabilities / int64 tokens"}[args.op],
         "data": "synthetic (seeded counter-based generator, inputs/recipe.h; generated in HBM)",
         "config": {"workload": w["name"], "n_elements": n, "alg_bytes_per_step": alg,
                    "gelem_per_s": round(n / med / 1e9, 2),

@@ -23,6 +23,17 @@
  *     tracked through every split (P365).  Stable.  descending != 0 uses
  *     mask = bit (1-bits first): the exact reverse order, still stable.
  *
+ *   - scan_weighted_sample: App. B.3 (P463) "we scan w, and then, given a
+ *     uniform sample theta in [0,1] ... The output is an index i of w with
+ *     probability proportional to w_i" (inverse transform sampling): the
+ *     inclusive fp32 scan S of w is written to `cdf`, then
+ *     *index_out = min{ i : S_i > theta * S_{n-1} } (R14).
+ *   - scan_top_p_draw: the nucleus + draw step of top-p sampling (Sec. 5.5,
+ *     P299: "applies sort and scan on the token probability vector") on the
+ *     row scans C of the DESCENDING-sorted probabilities (scan_rows) and the
+ *     sort's permutation `order`: K = 1 + min{ j : C_j >= p } (all columns if
+ *     none), t = u_r * C_{K-1}, token = order[min{ k : C_k > t }] (R15).
+ *
  * Readings: a flag is true iff its int8 value is nonzero (R12);
  * the float code orders keys by the IEEE total order, -NaN < -inf < ... < -0
  * < +0 < ... < +inf < +NaN (R13).  Indices are int32: n must be < 2^31.
@@ -75,6 +86,23 @@ SCAN_API size_t scan_radix_sort_workspace_bytes(int64_t n, int key_type);
  * Errors as scan_split; SCAN_ERR_ARG also for an unknown key_type. */
 SCAN_API int scan_radix_sort(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, int key_type,
                              int descending, void* ws, size_t ws_bytes, void* stream);
+
+/* Weighted sampling (P463).  w [n] fp32 non-negative weights with a positive
+ * sum; cdf [n] fp32 device scratch that receives the inclusive scan; ws a scan
+ * workspace of scan_workspace_bytes(SCAN_F32_F32, n) bytes; index_out ONE
+ * device int64.  theta in [0, 1) is the uniform draw (an input, R16). */
+SCAN_API int scan_weighted_sample(const float* w, int64_t n, double theta, int64_t* index_out, float* cdf,
+                                  void* ws, size_t ws_bytes, void* stream);
+
+/* Top-p draw on `rows` rows.  cdf: row r at cdf + r*cdf_row_stride, the
+ * inclusive scan of row r's probabilities sorted in descending order; order:
+ * row r at order + r*order_row_stride, int64 original column of every sorted
+ * entry; u [rows] fp32 uniform draws in [0, 1); p the nucleus mass.
+ * Outputs: token_out [rows] int64 sampled column, kept_out NULL or [rows]
+ * int32 nucleus size K.  Strides are in elements, >= cols. */
+SCAN_API int scan_top_p_draw(const float* cdf, const int64_t* order, int64_t rows, int64_t cols,
+                             int64_t cdf_row_stride, int64_t order_row_stride, float p, const float* u,
+                             int64_t* token_out, int32_t* kept_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -15,6 +15,8 @@ Public API (names follow the C ABI):
     sharded_inclusive / sharded_exclusive     -- see paper_2505_15112_b200.dist
     split(x, flags) / compress(x, flags)      -- P281-285 SplitInd / compress
     radix_sort(keys, descending=False)        -- P286-287 LSB radix sort by splits
+    weighted_sample(w, theta)                 -- P463 inverse transform on scan(w)
+    top_p_sample(probs, p, u)                 -- P298-299 sort + row scan + nucleus draw
 """
 from __future__ import annotations
 
@@ -92,6 +94,10 @@ def load() -> ctypes.CDLL:
         L.scan_radix_sort_workspace_bytes.restype = SZ
         L.scan_radix_sort.argtypes = [P, P, P, I64, I, I, P, SZ, P]
         L.scan_radix_sort.restype = I
+        L.scan_weighted_sample.argtypes = [P, I64, ctypes.c_double, P, P, P, SZ, P]
+        L.scan_weighted_sample.restype = I
+        L.scan_top_p_draw.argtypes = [P, P, I64, I64, I64, I64, ctypes.c_float, P, P, P, P]
+        L.scan_top_p_draw.restype = I
         _lib = L
     return _lib
 
@@ -328,3 +334,42 @@ def radix_sort(keys: torch.Tensor, descending: bool = False, out=None, idx_out=N
     _check(L.scan_radix_sort(_ptr(keys), _ptr(kout), _ptr(idx), n, kt, int(bool(descending)),
                              ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)), "scan_radix_sort")
     return kout, idx
+
+
+def weighted_sample(w: torch.Tensor, theta: float, cdf=None, stream=None) -> torch.Tensor:
+    """P463 weighted sampling: scan w (fp32, our scan) and draw the index whose
+    cumulative interval contains theta * sum(w) (R14).  Returns a 1-element
+    int64 CUDA tensor; `cdf` (optional, [n] fp32) receives the scan."""
+    if not w.is_cuda or w.dtype != torch.float32:
+        raise ScanError("weights must be a CUDA float32 tensor (there is no CPU path)")
+    w = w.reshape(-1).contiguous()
+    n = w.numel()
+    cdf = torch.empty_like(w) if cdf is None else cdf
+    out = torch.empty(1, dtype=torch.int64, device=w.device)
+    L = load()
+    ws = workspace(L.scan_workspace_bytes(SCAN_F32_F32, n), w.device, stream)
+    _check(L.scan_weighted_sample(_ptr(w), n, float(theta), _ptr(out), _ptr(cdf), ctypes.c_void_p(ws.ptr),
+                                  ws.nbytes, _stream_ptr(stream)), "scan_weighted_sample")
+    return out
+
+
+def top_p_sample(probs: torch.Tensor, p: float, u: torch.Tensor, stream=None):
+    """P298-299 top-p (nucleus) sampling of every row of `probs` [rows, cols]:
+    descending sort (torch.sort, a library segmented sort), our row scan
+    (scan_rows, P437) of the sorted probabilities, then our nucleus + inverse
+    transform draw (scan_top_p_draw, R15) with the uniform draws u [rows].
+
+    Returns (tokens int64 [rows], nucleus sizes int32 [rows])."""
+    if not (probs.is_cuda and u.is_cuda) or probs.dtype != torch.float32 or u.dtype != torch.float32:
+        raise ScanError("probs and u must be CUDA float32 tensors (there is no CPU path)")
+    if probs.dim() != 2 or u.numel() != probs.shape[0]:
+        raise ScanError("probs must be [rows, cols] and u [rows]")
+    R, C = probs.shape
+    sp, order = torch.sort(probs, dim=1, descending=True, stable=True)
+    cdf = rows(sp)
+    tok = torch.empty(R, dtype=torch.int64, device=probs.device)
+    kept = torch.empty(R, dtype=torch.int32, device=probs.device)
+    _check(load().scan_top_p_draw(_ptr(cdf), _ptr(order), R, C, cdf.stride(0), order.stride(0), float(p),
+                                  _ptr(u.contiguous()), _ptr(tok), _ptr(kept), _stream_ptr(stream)),
+           "scan_top_p_draw")
+    return tok, kept

@@ -3,6 +3,7 @@
 // and launch counter.  Host code only: argument checks and launches.
 #pragma once
 #include "../../include/scan_ops.h"
+#include "sample.cuh"
 #include "split.cuh"
 
 namespace {
@@ -206,6 +207,35 @@ int scan_radix_sort(const void* keys, void* keys_out, int32_t* idx_out, int64_t 
         src_i = di_;
     }
     return SCAN_OK;
+}
+
+int scan_weighted_sample(const float* w, int64_t n, double theta, int64_t* index_out, float* cdf, void* ws,
+                         size_t ws_bytes, void* stream)
+{
+    if (n <= 0 || w == nullptr || index_out == nullptr || cdf == nullptr || !(theta >= 0.0 && theta <= 1.0))
+        return SCAN_ERR_ARG;
+    int st = scan_1d(w, cdf, n, SCAN_F32_F32, nullptr, ws, ws_bytes, stream, 0);
+    if (st != SCAN_OK) return st;
+    scan::sample::k_weighted_draw<<<1, scan::sample::kThreads, 0, (cudaStream_t)stream>>>(cdf, n, theta, index_out);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+}
+
+int scan_top_p_draw(const float* cdf, const int64_t* order, int64_t rows, int64_t cols, int64_t cdf_row_stride,
+                    int64_t order_row_stride, float p, const float* u, int64_t* token_out, int32_t* kept_out,
+                    void* stream)
+{
+    if (rows < 0 || cols < 0 || cdf_row_stride < cols || order_row_stride < cols) return SCAN_ERR_ARG;
+    if (rows == 0) return SCAN_OK;
+    if (cols == 0 || cdf == nullptr || order == nullptr || u == nullptr || token_out == nullptr) return SCAN_ERR_ARG;
+    if (rows > 0x7fffffff) return SCAN_ERR_ARG;
+    DevInfo di;
+    int st = dev_info(di);
+    if (st != SCAN_OK) return st;
+    scan::sample::k_top_p_draw<<<(unsigned)rows, scan::sample::kThreads, 0, (cudaStream_t)stream>>>(
+        cdf, order, cols, cdf_row_stride, order_row_stride, p, u, token_out, kept_out);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
 }
 
 }  // extern "C"

@@ -139,3 +139,61 @@ def test_radix_sort_matches_torch_sort_stable(cuda):
             out, idx = cuda.radix_sort(k, descending=desc)
             ref, ridx = torch.sort(k, stable=True, descending=desc)
             assert torch.equal(out, ref) and torch.equal(idx.to(torch.int64), ridx)
+
+
+# ---------------------------------------------------------- sampling (P463, P299)
+def _valid_interval(S64, j, t, tol):
+    """j is a valid inverse-transform draw for threshold t on the fp64 prefix
+    sums S64 (within the scan tolerance tol): S_{j-1} <= t < S_j."""
+    lo = S64[j - 1] if j > 0 else 0.0
+    return lo <= t + tol and S64[j] > t - tol
+
+
+def test_weighted_sample_parity(cuda, oracle, inputs_mod):
+    rng = np.random.default_rng(21)
+    for n in (1, 17, 8193, 100003, 1 << 20):
+        w = rng.random(n).astype(np.float32)
+        w[rng.random(n) < 0.1] = 0
+        if w.sum() == 0:
+            w[0] = 1
+        wd = torch.from_numpy(w).cuda()
+        S64 = np.cumsum(w.astype(np.float64))
+        tol = 1e-6 * S64[-1] + 1e-6
+        same = 0
+        thetas = [0.0, 0.5, 0.999, *rng.random(5)]
+        for th in thetas:
+            got = int(cuda.weighted_sample(wd, th).item())
+            ref = oracle.weighted_sample(w, th)
+            assert 0 <= got < n and w[got] > 0
+            assert _valid_interval(S64, got, th * S64[-1], tol), (n, th, got, ref)
+            same += got == ref
+        assert same >= len(thetas) - 1  # differs only when t sits within rounding of a boundary
+
+
+def test_top_p_parity(cuda, oracle, inputs_mod):
+    """C4-style rows (softmax(4 z)), several p; token and nucleus size match the
+    oracle except where a threshold sits within float rounding of a boundary,
+    and are always valid draws within the scan tolerance."""
+    R, C = 64, 131072
+    P = inputs_mod.fill_host(inputs_mod.F32_SOFTMAX, 3, 0, R, C)
+    Pd = torch.from_numpy(P).cuda()
+    rng = np.random.default_rng(3)
+    u = rng.random(R).astype(np.float32)
+    ud = torch.from_numpy(u).cuda()
+    for p in (0.0, 0.5, 0.9, 0.95, 2.0):
+        tok, kept = cuda.top_p_sample(Pd, p, ud)
+        tok, kept = tok.cpu().numpy(), kept.cpu().numpy()
+        agree = 0
+        for r in range(R):
+            rt, rk = oracle.top_p_sample(P[r], p, float(u[r]))
+            order = np.argsort(-P[r].astype(np.float64), kind="stable")
+            C64 = np.cumsum(P[r][order].astype(np.float64))
+            tol = 1e-6 * C64[-1] + 1e-6
+            K = int(kept[r])
+            # nucleus: smallest prefix with mass >= p (R15), within tolerance
+            assert K >= 1 and (K == C or C64[K - 1] >= p - tol)
+            assert K == 1 or C64[K - 2] < p + tol
+            rank = int(np.nonzero(order == tok[r])[0][0])
+            assert rank < K and _valid_interval(C64, rank, float(u[r]) * C64[K - 1], tol)
+            agree += (tok[r] == rt) and (K == rk)
+        assert agree >= R - 2, (p, agree)
