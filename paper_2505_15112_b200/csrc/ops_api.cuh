@@ -17,7 +17,9 @@ constexpr size_t kSplitArrays = kWsDescOffset;  // counts[ntiles] then offs[ntil
 
 int64_t split_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
 
-size_t split_ws_bytes(int64_t n) { return kSplitArrays + (size_t)split_tiles(n) * 8 + 64; }
+int64_t split_tiles4(int64_t n) { return (split_tiles(n) + 3) & ~(int64_t)3; }  // 16-byte aligned arrays
+
+size_t split_ws_bytes(int64_t n) { return kSplitArrays + (size_t)split_tiles4(n) * 8 + 64; }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
@@ -102,7 +104,7 @@ void split_ws_setup(SplitParams& p, void* ws, int64_t n)
     uint8_t* w = (uint8_t*)ws;
     p.hdr = reinterpret_cast<uint32_t*>(w + kSplitHdr);
     p.counts = reinterpret_cast<uint32_t*>(w + kSplitArrays);
-    p.offs = p.counts + split_tiles(n);
+    p.offs = p.counts + split_tiles4(n);
     p.n = n;
     p.ntiles = (int)split_tiles(n);
 }

@@ -86,8 +86,10 @@ __device__ __forceinline__ uint32_t mask16(const SplitParams& p, const uint4& fq
         const uint32_t f[4] = {fq.x, fq.y, fq.z, fq.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const uint32_t nz = (((f[j] & 0x7f7f7f7fu) + 0x7f7f7f7fu) | f[j]) & 0x80808080u;  // nonzero bytes
-            bits |= (((nz >> 7) & 1u) | ((nz >> 14) & 2u) | ((nz >> 21) & 4u) | ((nz >> 28) & 8u)) << (4 * j);
+            // 0x80 in every nonzero byte; the multiply moves bits 7/15/23/31 to
+            // 28/29/30/31 without overlapping partial products (no carries)
+            const uint32_t nz = __vcmpne4(f[j], 0u) & 0x80808080u;
+            bits |= ((nz * 0x00204081u) >> 28) << (4 * j);
         }
     } else {
         const uint32_t inv = p.descending ? 0u : 1u;
@@ -222,15 +224,23 @@ __global__ void __launch_bounds__(kThreads) k_split_count(const SplitParams p)
     if (!s_last) return;
     __threadfence();
     uint64_t carry = 0;
-    for (int base = 0; base < p.ntiles; base += kThreads * 4) {
-        uint32_t v[4];
+    constexpr int kPerT = 16;  // counts per thread per pass (4 x 16-byte loads)
+    for (int base = 0; base < p.ntiles; base += kThreads * kPerT) {
+        uint32_t v[kPerT];
         uint32_t s = 0;
+        const int i0 = base + tid * kPerT;
+        if (i0 + kPerT <= p.ntiles) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = base + tid * 4 + k;
-            v[k] = i < p.ntiles ? __ldcg(&p.counts[i]) : 0u;
-            s += v[k];
+            for (int k = 0; k < kPerT; k += 4) {
+                const uint4 q = __ldcg(reinterpret_cast<const uint4*>(p.counts + i0 + k));
+                v[k] = q.x; v[k + 1] = q.y; v[k + 2] = q.z; v[k + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kPerT; ++k) v[k] = i0 + k < p.ntiles ? __ldcg(&p.counts[i0 + k]) : 0u;
         }
+#pragma unroll
+        for (int k = 0; k < kPerT; ++k) s += v[k];
         uint32_t incl = s;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -240,18 +250,32 @@ __global__ void __launch_bounds__(kThreads) k_split_count(const SplitParams p)
         __syncthreads();
         if (lane == 31) s_red[warp] = incl;
         __syncthreads();
-        uint32_t wpre = 0, tot = 0;
-        for (int w = 0; w < kWarps; ++w) {
-            const uint32_t x = s_red[w];
-            if (w < warp) wpre += x;
-            tot += x;
-        }
-        uint64_t run = carry + wpre + (incl - s);
+        uint32_t xw = lane < kWarps ? s_red[lane] : 0u;
+        uint32_t xi = xw;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int i = base + tid * 4 + k;
-            if (i < p.ntiles) p.offs[i] = (uint32_t)run;
-            run += v[k];
+        for (int d = 1; d < kWarps; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, xi, d);
+            if (lane >= d) xi += y;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, xi, kWarps - 1);
+        const uint32_t wpre = __shfl_sync(0xffffffffu, xi - xw, warp);
+        uint64_t run = carry + wpre + (incl - s);
+        if (i0 + kPerT <= p.ntiles) {
+            uint32_t o[kPerT];
+#pragma unroll
+            for (int k = 0; k < kPerT; ++k) {
+                o[k] = (uint32_t)run;
+                run += v[k];
+            }
+#pragma unroll
+            for (int k = 0; k < kPerT; k += 4)
+                *reinterpret_cast<uint4*>(p.offs + i0 + k) = make_uint4(o[k], o[k + 1], o[k + 2], o[k + 3]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < kPerT; ++k) {
+                if (i0 + k < p.ntiles) p.offs[i0 + k] = (uint32_t)run;
+                run += v[k];
+            }
         }
         carry += tot;
     }
@@ -380,6 +404,47 @@ __device__ __forceinline__ void write_run(uint8_t* z, int32_t* idx, uint64_t g0,
     }
 }
 
+// Packed staging (payload << 16 | local index): write a run of `len` staged
+// words (staging index s0.., global index g0.., s0 == g0 mod 4); 4-element
+// groups go out as one payload vector (8 B fp16 / 4 B int8) and one 16-byte
+// index vector; idx = tile base + local index.
+template <int ES>
+__device__ __forceinline__ void write_run_packed(uint8_t* z, int32_t* idx, uint64_t g0, int32_t t0, const uint32_t* st,
+                                                 int s0, int len, int tid)
+{
+    int head = (int)((4 - (int)(g0 & 3)) & 3);
+    head = head < len ? head : len;
+    const int nv = (len - head) >> 2;
+    const int body_end = head + nv * 4;
+    auto scalar = [&](int i) {
+        const uint32_t w = st[s0 + i];
+        const uint64_t d = g0 + (uint64_t)i;
+        if constexpr (ES == 2) reinterpret_cast<uint16_t*>(z)[d] = (uint16_t)(w >> 16);
+        else z[d] = (uint8_t)(w >> 16);
+        if (idx) idx[d] = t0 + (int32_t)(w & 0xffffu);
+    };
+    if (tid < head) scalar(tid);
+    const int tail = len - body_end;
+    if (tid < tail) scalar(body_end + tid);
+    const uint4* sv = reinterpret_cast<const uint4*>(st + s0 + head);
+    const uint64_t gb = g0 + head;
+    for (int v = tid; v < nv; v += kThreads) {
+        const uint4 q = sv[v];
+        if constexpr (ES == 2) {
+            const uint2 pay = make_uint2(__byte_perm(q.x, q.y, 0x7632), __byte_perm(q.z, q.w, 0x7632));
+            *reinterpret_cast<uint2*>(z + (gb + 4 * (uint64_t)v) * 2) = pay;
+        } else {
+            const uint32_t pay = __byte_perm(__byte_perm(q.x, q.y, 0x0062), __byte_perm(q.z, q.w, 0x0062), 0x5410);
+            *reinterpret_cast<uint32_t*>(z + gb + 4 * (uint64_t)v) = pay;
+        }
+        if (idx) {
+            const uint4 iv = make_uint4(t0 + (q.x & 0xffffu), t0 + (q.y & 0xffffu), t0 + (q.z & 0xffffu),
+                                        t0 + (q.w & 0xffffu));
+            *reinterpret_cast<uint4*>(idx + gb + 4 * (uint64_t)v) = iv;
+        }
+    }
+}
+
 // ---- pass 2, TMA variant: a producer warp streams tiles into a shared-memory
 // ring (cp.async.bulk, mbarrier completion), so the HBM latency is hidden by
 // the ring depth instead of occupancy; 16 compute warps scan, stage and write.
@@ -394,7 +459,9 @@ struct TmaCfg {
     static constexpr int kIdxB = IDX_IN ? kTile * 4 : 0;
     static constexpr int kSlot = kFlagB + kPayB + kIdxB;
     static constexpr int kSlack = 64;                         // alignment shifts of the two runs
-    static constexpr int kStage = (kTile + kSlack) * (ES + 4);
+    // !IDX_IN and ES <= 2: one packed word per element, (payload << 16) | local index
+    static constexpr bool kPack = !IDX_IN && ES <= 2;
+    static constexpr int kStage = kPack ? (kTile + kSlack) * 4 : (kTile + kSlack) * (ES + 4);
     static constexpr int kNB = (200 * 1024 - kStage) / kSlot > 4 ? 4 : (200 * 1024 - kStage) / kSlot;
     static constexpr size_t kSmem = (size_t)kNB * kSlot + kStage + 128;
 };
@@ -510,37 +577,59 @@ __global__ void __launch_bounds__(TmaCfg<SRC, ES, IDX_IN>::kThreadsT, 1) k_split
         }
         if (cl == 31) s_red[par][cw] = incl;
         ptx::named_bar_sync(1, kThreads);  // also: the previous tile's staging has been written out
-        uint32_t wpre = 0, ct = 0;
+        uint32_t xw = cl < kWarps ? s_red[par][cl] : 0u;  // warp totals, scanned by every warp
+        uint32_t xi = xw;
 #pragma unroll
-        for (int k = 0; k < kWarps; ++k) {
-            const uint32_t x = s_red[par][k];
-            if (k < cw) wpre += x;
-            ct += x;
+        for (int d = 1; d < kWarps; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, xi, d);
+            if (cl >= d) xi += y;
         }
-        // Staging positions are shifted so that staging index == global index
-        // (mod VE): the middle of each run is then written with 16-byte stores.
-        constexpr int VE = 16 / ES;  // elements per 16-byte payload vector (ES <= 4)
+        const uint32_t ct = __shfl_sync(0xffffffffu, xi, kWarps - 1);
+        const uint32_t wpre = __shfl_sync(0xffffffffu, xi - xw, cw);
+        const uint32_t lt = wpre + incl - c;              // trues before this thread in the tile
+        const uint32_t lf = (uint32_t)(ct_ * kPer) - lt;  // falses before this thread
         const uint64_t off_t = p.offs[t];
         const uint64_t fbase = T + (uint64_t)t0 - off_t;
-        const int sh_t = (int)(off_t % VE);
-        const int fst = ((sh_t + (int)ct + VE - 1) / VE) * VE + (int)(fbase % VE);
-        const uint32_t lt = wpre + incl - c;
-        const uint32_t lf = (uint32_t)(ct_ * kPer) - lt;
-        uint32_t rt_ = sh_t + lt, rf = fst + lf;
+        if constexpr (C::kPack) {
+            // staging index == global index (mod 4): 4-element groups store as one vector
+            uint32_t* const s_pk = reinterpret_cast<uint32_t*>(s_stage);
+            const int sh_t = (int)(off_t & 3);
+            const int fst = ((sh_t + (int)ct + 3) & ~3) + (int)(fbase & 3);
+            const uint32_t tb = sh_t + lt, fb = fst + lf;
 #pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-            if (j >= m) break;
-            const bool tr = (bits >> j) & 1u;
-            const uint32_t pos = tr ? rt_++ : rf++;
-            if constexpr (ES == 1) s_stage[pos] = (uint8_t)(L.w[j >> 2] >> (8 * (j & 3)));
-            else if constexpr (ES == 2) reinterpret_cast<uint16_t*>(s_stage)[pos] = (uint16_t)(L.w[j >> 1] >> (16 * (j & 1)));
-            else reinterpret_cast<uint32_t*>(s_stage)[pos] = L.w[j];
-            s_idx[pos] = L.ix[j];
+            for (int j = 0; j < kPer; ++j) {
+                if (j >= m) break;
+                const uint32_t below = __popc(bits & ((1u << j) - 1u));  // trues before j in this thread
+                const uint32_t pos = ((bits >> j) & 1u) ? tb + below : fb + (uint32_t)j - below;
+                uint32_t pay;
+                if constexpr (ES == 2) pay = (L.w[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+                else pay = (L.w[j >> 2] >> (8 * (j & 3))) & 0xffu;
+                s_pk[pos] = (pay << 16) | (uint32_t)(ct_ * kPer + j);
+            }
+            ptx::named_bar_sync(1, kThreads);
+            write_run_packed<ES>(zb, p.idx_out, off_t, (int32_t)t0, s_pk, sh_t, (int)ct, ct_);
+            if (!p.compress) write_run_packed<ES>(zb, p.idx_out, fbase, (int32_t)t0, s_pk, fst, mt - (int)ct, ct_);
+        } else {
+            // Staging positions are shifted so that staging index == global index
+            // (mod VE): the middle of each run is then written with 16-byte stores.
+            constexpr int VE = 16 / ES;  // elements per 16-byte payload vector (ES <= 4)
+            const int sh_t = (int)(off_t % VE);
+            const int fst = ((sh_t + (int)ct + VE - 1) / VE) * VE + (int)(fbase % VE);
+            uint32_t rt_ = sh_t + lt, rf = fst + lf;
+#pragma unroll
+            for (int j = 0; j < kPer; ++j) {
+                if (j >= m) break;
+                const bool tr = (bits >> j) & 1u;
+                const uint32_t pos = tr ? rt_++ : rf++;
+                if constexpr (ES == 1) s_stage[pos] = (uint8_t)(L.w[j >> 2] >> (8 * (j & 3)));
+                else if constexpr (ES == 2) reinterpret_cast<uint16_t*>(s_stage)[pos] = (uint16_t)(L.w[j >> 1] >> (16 * (j & 1)));
+                else reinterpret_cast<uint32_t*>(s_stage)[pos] = L.w[j];
+                s_idx[pos] = L.ix[j];
+            }
+            ptx::named_bar_sync(1, kThreads);
+            write_run<ES>(zb, p.idx_out, off_t, s_stage, s_idx, sh_t, (int)ct, ct_);
+            if (!p.compress) write_run<ES>(zb, p.idx_out, fbase, s_stage, s_idx, fst, mt - (int)ct, ct_);
         }
-        ptx::named_bar_sync(1, kThreads);
-
-        write_run<ES>(zb, p.idx_out, off_t, s_stage, s_idx, sh_t, (int)ct, ct_);
-        if (!p.compress) write_run<ES>(zb, p.idx_out, fbase, s_stage, s_idx, fst, mt - (int)ct, ct_);
         // the next tile's first named barrier orders these staging reads before its writes
     }
 }
