@@ -138,6 +138,29 @@ SCAN_API int scan_total(const void* in, int64_t n, int dtype, void* total_out, v
 SCAN_API int scan_carry_from_totals(const void* totals, int G, int rank, int dtype, void* carry_out,
                            void* stream);
 
+/* Two-pass sharded scan: the per-GPU work of the multi-GPU Reduce-Scan-Scan
+ * (P73, Sec. 2.1: "a block-level reduction first, followed by a scan of the
+ * block-level reductions and a final scan of each block"), with blocks of
+ * 131,072 elements.
+ *   scan_shard_reduce: one read of the shard; *total_out = sum of the n
+ *     elements (int64 / double, as scan_total, fixed order) and the block sums
+ *     and their exclusive prefix are kept in `ws`.
+ *   scan_shard_scan: the scan of the SAME shard (same n, dtype and ws, after
+ *     scan_shard_reduce in stream order) seeded with carry_in (device pointer,
+ *     NULL = 0; the sum of the lower shards, e.g. from scan_carry_from_totals):
+ *     every block starts from carry_in + its prefix, so the pass is a pure
+ *     stream (the batched row kernel), inclusive or exclusive.  Results equal
+ *     scan_inclusive / scan_exclusive with the same carry_in (bit-exact for
+ *     integers, within the float tolerance).  Unaligned or in-place buffers
+ *     fall back to the single-pass scan.
+ * ws: scan_shard_workspace_bytes(dtype, n) bytes, initialised once with
+ * scan_workspace_init; one workspace per shard in flight. */
+SCAN_API size_t scan_shard_workspace_bytes(int dtype, int64_t n);
+SCAN_API int scan_shard_reduce(const void* in, int64_t n, int dtype, void* total_out, void* ws, size_t ws_bytes,
+                               void* stream);
+SCAN_API int scan_shard_scan(const void* in, void* out, int64_t n, int dtype, int exclusive, const void* carry_in,
+                             void* ws, size_t ws_bytes, void* stream);
+
 /* End-to-end scan of an array in HOST memory (pinned for full speed): the
  * array is streamed through the GPU in chunks of `chunk_elems` elements with
  * the host->device copy of chunk i+1, the scan of chunk i and the

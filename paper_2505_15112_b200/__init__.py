@@ -85,6 +85,12 @@ def load() -> ctypes.CDLL:
         L.scan_host_stage_bytes.restype = SZ
         L.scan_host.argtypes = [P, P, I64, I, I, I64, P, SZ, P, SZ, P]
         L.scan_host.restype = I
+        L.scan_shard_workspace_bytes.argtypes = [I, I64]
+        L.scan_shard_workspace_bytes.restype = SZ
+        L.scan_shard_reduce.argtypes = [P, I64, I, P, P, SZ, P]
+        L.scan_shard_reduce.restype = I
+        L.scan_shard_scan.argtypes = [P, P, I64, I, I, P, P, SZ, P]
+        L.scan_shard_scan.restype = I
         # include/scan_ops.h
         L.scan_split_workspace_bytes.argtypes = [I64]
         L.scan_split_workspace_bytes.restype = SZ
@@ -265,6 +271,43 @@ def host_scan(h_in: torch.Tensor, h_out=None, exclusive: bool = False, chunk: in
                        int(bool(exclusive)), chunk, _ptr(stage), sb, ctypes.c_void_p(ws.ptr), ws.nbytes,
                        _stream_ptr(stream)), "scan_host")
     return h_out
+
+
+def shard_workspace(x: torch.Tensor, stream=None) -> Workspace:
+    """A fresh initialised workspace for one shard of the two-pass sharded scan
+    (it keeps the shard's block sums between shard_reduce and shard_scan)."""
+    dt, _, _ = _prep(x)
+    return Workspace(load().scan_shard_workspace_bytes(dt, x.numel()), x.device, stream)
+
+
+def shard_reduce(x: torch.Tensor, ws: Workspace | None = None, out=None, stream=None) -> torch.Tensor:
+    """Pass 1 of the sharded scan (P73 block-level reduction): the shard total
+    (1-element int64 / float64 CUDA tensor); block sums stay in `ws`."""
+    dt, _, cdt = _prep(x)
+    n = x.reshape(-1).numel()
+    L = load()
+    ws = ws if ws is not None else workspace(L.scan_shard_workspace_bytes(dt, n), x.device, stream)
+    out = torch.empty(1, dtype=cdt, device=x.device) if out is None else out
+    _check(L.scan_shard_reduce(_ptr(x), n, dt, _ptr(out), ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)),
+           "scan_shard_reduce")
+    return out
+
+
+def shard_scan(x: torch.Tensor, exclusive: bool = False, carry_in=None, ws: Workspace | None = None, out=None,
+               stream=None) -> torch.Tensor:
+    """Pass 2 of the sharded scan: scan of the shard given to shard_reduce (same
+    `ws`), every block starting from carry_in + its block prefix."""
+    dt, odt, cdt = _prep(x)
+    x = x.reshape(-1)
+    n = x.numel()
+    if carry_in is not None and (carry_in.dtype != cdt or not carry_in.is_cuda):
+        raise ScanError(f"carry_in must be a CUDA {cdt} tensor")
+    out = torch.empty(n, dtype=odt, device=x.device) if out is None else out
+    L = load()
+    ws = ws if ws is not None else workspace(L.scan_shard_workspace_bytes(dt, n), x.device, stream)
+    _check(L.scan_shard_scan(_ptr(x), _ptr(out), n, dt, int(bool(exclusive)), _ptr(carry_in),
+                             ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)), "scan_shard_scan")
+    return out
 
 
 def launch_count() -> int:

@@ -32,6 +32,10 @@ struct RowParams {
     int64_t in_stride;   // elements
     int tiles_per_row;
     int exclusive;
+    // Sharded scan pass 2 (shard.cuh): row r starts from carry_in + row_pre[r]
+    // (int64 for integer dtypes, double for floats); both NULL for plain rows.
+    const void* row_pre;
+    const void* carry_in;
 };
 
 template <int DT, int NC, int GPW, int NB>
@@ -192,7 +196,18 @@ __global__ void __launch_bounds__((2 + NC) * 32, 1) k_rowscan16(const __grid_con
                 break;
             }
             const int k = s_k[s];
-            if (k == 0) carry = Carry(0);  // a new row starts from zero (P437)
+            if (k == 0) {  // a new row starts from zero (P437) or from its block prefix (sharded pass 2)
+                carry = Carry(0);
+                if (p.row_pre != nullptr) {
+                    if constexpr (Tr::kFloat) {
+                        const double c0 = p.carry_in ? *reinterpret_cast<const double*>(p.carry_in) : 0.0;
+                        carry = c0 + reinterpret_cast<const double*>(p.row_pre)[row];
+                    } else {
+                        const long long c0 = p.carry_in ? *reinterpret_cast<const long long*>(p.carry_in) : 0ll;
+                        carry = (Carry)(uint32_t)(uint64_t)(c0 + reinterpret_cast<const long long*>(p.row_pre)[row]);
+                    }
+                }
+            }
             const int m = (int)(p.cols - (int64_t)k * TILE < TILE ? p.cols - (int64_t)k * TILE : TILE);
             uint8_t* const slot = ring + s * Cfg::kSlot;
 

@@ -377,6 +377,8 @@ struct RowVariant {
         p.in_stride = sp.in_stride;
         p.tiles_per_row = (int)((sp.seg_len + Cfg::kTile - 1) / Cfg::kTile);
         p.exclusive = sp.exclusive;
+        p.row_pre = sp.row_pre;
+        p.carry_in = sp.row_pre ? sp.carry_in : nullptr;
         int64_t grid = di.sms;
         if (grid > sp.num_segs) grid = sp.num_segs;
         k_rowscan16<DT, NC, GPW, NB><<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(p);
@@ -792,3 +794,5 @@ int scan_host(const void* h_in, void* h_out, int64_t n, int dtype, int exclusive
 
 // ---- scan-based operators (include/scan_ops.h) ----
 #include "ops_api.cuh"
+// ---- two-pass sharded scan (multi-GPU Reduce-Scan-Scan, include/scan.h) ----
+#include "shard_api.cuh"

@@ -381,7 +381,8 @@ struct ScanParams {
     int64_t out_stride;     // elements between segment starts (output)
     int64_t tiles_per_seg;
     int64_t num_tiles;
-    const void* carry_in;   // nullable; applies to segment 0 (1-D API only)
+    const void* carry_in;   // nullable; applies to segment 0 (1-D API only; rows: added to row_pre)
+    const void* row_pre;    // nullable; rows kernel: per-row start value (sharded scan pass 2)
     uint8_t* ws;            // workspace (unused when static_sched)
     int exclusive;
     int tma_in;             // segment bases and strides 16-byte aligned (input)

@@ -1,0 +1,126 @@
+// shard.cuh -- pass 1 of the sharded (multi-GPU) scan: the block-level
+// reduction of Reduce-Scan-Scan (PAPER P73, Sec. 2.1: "a block-level
+// reduction first, followed by a scan of the block-level reductions and a
+// final scan of each block").
+//
+// A rank's shard cannot be scanned single-pass before the sums of the lower
+// shards are known, so it is read twice anyway.  Doing
+// the reduction per BLOCK (not just per shard) makes the second read a pure
+// stream: every block's starting value is known (carry of the lower shards +
+// exclusive prefix of the block sums), so pass 2 is the batched row kernel
+// (rowscan.cuh, one CTA per block-row, no grid barrier, no look-back) instead
+// of the single-GPU MCScan with its L2-resident re-read.
+//
+// k_block_sums: CTA c reduces blocks c, c + grid, ... (highest first, so the
+// shard's beginning -- which pass 2 reads first -- is read last and kept in L2
+// with evict_last), every element widened exactly to fp64 / int64, fixed
+// summation order (identical bits per call).  The last CTA scans the block
+// sums into pre[b] = sum of blocks < b and pre[nb] = the shard total.
+#pragma once
+#include <stdint.h>
+
+#include "ptx.cuh"
+#include "scan_kernels.cuh"
+
+namespace scan {
+namespace shard {
+
+constexpr int kThreads = 512;
+
+template <int DT>
+using SumT = typename std::conditional<Traits<DT>::kFloat, double, long long>::type;
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads) k_block_sums(const void* in_, int64_t n, int64_t blk, int64_t nb,
+                                                         SumT<DT>* bsum, SumT<DT>* pre, void* total_out,
+                                                         uint32_t* done)
+{
+    using Tr = Traits<DT>;
+    using In = typename Tr::In;
+    using Sum = SumT<DT>;
+    constexpr int VN = Vec16<In>::kN;  // elements per 16-byte vector
+    const In* in = reinterpret_cast<const In*>(in_);
+    const uint64_t pol = ptx::policy_evict_last();
+    __shared__ Sum s_part[kThreads / 32];
+    __shared__ bool s_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    for (int64_t b = nb - 1 - blockIdx.x; b >= 0; b -= gridDim.x) {
+        const int64_t lo = b * blk;
+        const int64_t m = n - lo < blk ? n - lo : blk;
+        // whole vectors (blocks start 16-byte aligned when the shard does)
+        const int64_t nv = (((uintptr_t)in_ & 15u) == 0) ? m / VN : 0;
+        const uint4* v = reinterpret_cast<const uint4*>(in + lo);
+        Sum acc = 0;
+        int64_t i = tid;
+        for (; i + 3 * kThreads < nv; i += 4 * kThreads) {
+            const uint4 a = ptx::ld_keep_v4(v + i, pol);
+            const uint4 b1 = ptx::ld_keep_v4(v + i + kThreads, pol);
+            const uint4 c = ptx::ld_keep_v4(v + i + 2 * kThreads, pol);
+            const uint4 d = ptx::ld_keep_v4(v + i + 3 * kThreads, pol);
+            acc += sum_vec16<DT, Sum>(a);
+            acc += sum_vec16<DT, Sum>(b1);
+            acc += sum_vec16<DT, Sum>(c);
+            acc += sum_vec16<DT, Sum>(d);
+        }
+        for (; i < nv; i += kThreads) acc += sum_vec16<DT, Sum>(ptx::ld_keep_v4(v + i, pol));
+        for (int64_t j = nv * VN + tid; j < m; j += kThreads) acc += to_sum<Sum>(widen(in[lo + j]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        __syncthreads();
+        if (lane == 0) s_part[warp] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            Sum t = 0;
+            for (int w = 0; w < kThreads / 32; ++w) t += s_part[w];
+            bsum[b] = t;
+        }
+    }
+    // last CTA: exclusive scan of the block sums (fixed tree order), total
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    Sum carry = 0;
+    for (int64_t base = 0; base < nb; base += kThreads) {
+        const int64_t i = base + tid;
+        const Sum x = i < nb ? ((volatile Sum*)bsum)[i] : Sum(0);
+        Sum incl = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const Sum y = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += y;
+        }
+        __syncthreads();
+        if (lane == 31) s_part[warp] = incl;
+        __syncthreads();
+        Sum wpre = 0, tot = 0;
+        for (int w = 0; w < kThreads / 32; ++w) {
+            const Sum y = s_part[w];
+            if (w < warp) wpre += y;
+            tot += y;
+        }
+        Sum ex = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) ex = Sum(0);
+        if (i < nb) pre[i] = carry + (wpre + ex);
+        carry += tot;
+    }
+    if (tid == 0) {
+        pre[nb] = carry;
+        *reinterpret_cast<Sum*>(total_out) = carry;
+        *done = 0;
+    }
+}
+
+// carry_out = carry_in (nullable) + pre[idx]: the start value of a trailing
+// partial block handed to the 1-D scan.
+template <typename Sum>
+__global__ void k_carry_plus(const Sum* carry_in, const Sum* pre, int64_t idx, Sum* carry_out)
+{
+    if (threadIdx.x == 0) *carry_out = (carry_in ? *carry_in : Sum(0)) + pre[idx];
+}
+
+}  // namespace shard
+}  // namespace scan

@@ -6,11 +6,13 @@ at device level (PAPER.md P73, Sec. 2.1: "the RSS approach makes a block-level
 reduction first, followed by a scan of the block-level reductions and a final
 scan of each block"), with GPUs as the blocks:
 
-  1. scan_total            the shard's sum (int64 / fp64), one read of the shard
+  1. scan_shard_reduce     one read of the shard: its sum (int64 / fp64) and the
+                           sums of its 131,072-element blocks, kept on the device
   2. all_gather (NCCL)     G sums over NVLink / NVSwitch (8 bytes per rank)
   3. carry_from_totals     carry_r = totals[0] + ... + totals[r-1], fixed order
-  4. scan_inclusive/excl.  the shard scan, seeded with carry_r (fused into the
-                           kernel's block carries, so no extra pass)
+  4. scan_shard_scan       the shard scan: every block starts from carry_r + its
+                           block prefix (fused into the kernel's running carry),
+                           so the second read is a pure stream (row kernel)
 
 The host logic (shard bounds, the order of the exchange, the carry
 composition) lives in `rss_scan`, which takes the per-rank operations as
@@ -58,27 +60,44 @@ def _nccl_all_gather(group):
     return gather
 
 
-def _sharded(x_local: torch.Tensor, exclusive: bool, group=None, out=None):
-    from . import carry_from_totals, exclusive as scan_exc, inclusive as scan_inc, total
+_ws_cache: dict = {}
+
+
+def _shard_ws(x_local: torch.Tensor):
+    """One cached workspace per (device, stream, dtype, shard length): it carries
+    the block sums from pass 1 to pass 2 of a call and is reused by the next."""
+    from . import shard_workspace
+    key = (x_local.device.index, torch.cuda.current_stream(x_local.device).cuda_stream, x_local.dtype,
+           x_local.numel())
+    ws = _ws_cache.get(key)
+    if ws is None:
+        ws = _ws_cache[key] = shard_workspace(x_local)
+    return ws
+
+
+def _sharded(x_local: torch.Tensor, exclusive: bool, group=None, out=None, ws=None):
+    from . import carry_from_totals, shard_reduce, shard_scan
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
+    ws = ws if ws is not None else _shard_ws(x_local)
 
     def local_scan(x, exc, carry):
-        return (scan_exc if exc else scan_inc)(x, out=out, carry_in=carry)
+        return shard_scan(x, exc, carry_in=carry, ws=ws, out=out)
 
     y, _, _ = rss_scan(x_local, exclusive, rank, world,
-                       local_total=total,
+                       local_total=lambda x: shard_reduce(x, ws=ws),
                        all_gather=_nccl_all_gather(group),
                        carry_of=lambda totals, r: carry_from_totals(totals, r, x_local.dtype),
                        local_scan=local_scan)
     return y
 
 
-def sharded_inclusive(x_local: torch.Tensor, group=None, out=None) -> torch.Tensor:
-    """Inclusive scan of the array whose rank-r contiguous shard is x_local."""
-    return _sharded(x_local, False, group, out)
+def sharded_inclusive(x_local: torch.Tensor, group=None, out=None, ws=None) -> torch.Tensor:
+    """Inclusive scan of the array whose rank-r contiguous shard is x_local
+    (`ws`: a reusable paper_2505_15112_b200.shard_workspace for this shard)."""
+    return _sharded(x_local, False, group, out, ws)
 
 
-def sharded_exclusive(x_local: torch.Tensor, group=None, out=None) -> torch.Tensor:
+def sharded_exclusive(x_local: torch.Tensor, group=None, out=None, ws=None) -> torch.Tensor:
     """Exclusive scan of the array whose rank-r contiguous shard is x_local."""
-    return _sharded(x_local, True, group, out)
+    return _sharded(x_local, True, group, out, ws)

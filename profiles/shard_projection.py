@@ -1,0 +1,84 @@
+"""Per-GPU work of the sharded (multi-GPU) scan, timed on ONE B200, and the
+aggregate it projects to at G GPUs (weak in work per GPU, strong in n).
+
+Each "rank" of a G-way split of C5 (fp32, n = 2^32) / C3 (int8 -> int32
+exclusive, n = 2^30) does, on its own shard:
+  new:  scan_shard_reduce (one read) + carry_from_totals + scan_shard_scan
+        (row-kernel stream with per-block starts)       [paper_2505_15112_b200.dist]
+  old:  scan_total (one read) + carry_from_totals + scan with carry (MCScan)
+The NCCL all-gather of G x 8 bytes is not included (NVLink latency, ~10-20 us).
+CUDA events, median of 5 after 2 warm-ups; rank 1's shard (nonzero carry).
+
+    python profiles/shard_projection.py [C5|C3 ...]
+"""
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import inputs  # noqa: E402
+import paper_2505_15112_b200 as S  # noqa: E402
+from bench import peaks  # noqa: E402
+
+CFG = {"C5": (torch.float32, 1 << 32, inputs.F32_NORMAL, 4, False, 8),
+       "C3": (torch.int8, 1 << 30, inputs.I8_FLAG, 2, True, 5)}
+
+
+def timed(fn, reps=5, warm=2):
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3)
+    return statistics.median(ts)
+
+
+def main():
+    peak, _ = peaks()
+    out = []
+    for cfg in (sys.argv[1:] or ["C5", "C3"]):
+        dt, n, kind, seed, exc, bpe = CFG[cfg]
+        for G in (1, 2, 4, 8):
+            m = n // G
+            x = torch.empty(m, dtype=dt, device="cuda")
+            inputs.fill_device(kind, seed, m, m, 0, x)  # rank 1's shard
+            y = torch.empty(m, dtype=torch.int32 if dt == torch.int8 else torch.float32, device="cuda")
+            cdt = torch.int64 if dt == torch.int8 else torch.float64
+            totals = torch.ones(G, dtype=cdt, device="cuda")
+            ws = S.shard_workspace(x)
+
+            def new():
+                S.shard_reduce(x, ws=ws)
+                c = S.carry_from_totals(totals, min(1, G - 1), dt)
+                S.shard_scan(x, exc, carry_in=c, ws=ws, out=y)
+
+            def old():
+                S.total(x)
+                c = S.carry_from_totals(totals, min(1, G - 1), dt)
+                (S.exclusive if exc else S.inclusive)(x, out=y, carry_in=c)
+
+            def single():
+                (S.exclusive if exc else S.inclusive)(x, out=y)
+
+            rec = {"config": cfg, "G": G, "shard_elems": m}
+            for name, fn in (("rss_blocks", new), ("rss_mcscan", old), ("single_pass", single)):
+                t = timed(fn)
+                rec[name] = {"per_gpu_us": round(t * 1e6, 1), "per_gpu_pct_alg": round(100 * m * bpe / t / 1e9 / peak, 1),
+                             "aggregate_GBps": round(G * m * bpe / t / 1e9, 0)}
+            print(json.dumps(rec), flush=True)
+            out.append(rec)
+            del x, y, ws
+            torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()

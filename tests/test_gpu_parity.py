@@ -252,7 +252,7 @@ def test_large_ragged(cuda, oracle, inputs_mod, dt):
         assert_parity(oracle, got, oracle_1d(oracle, x, dt, exclusive, carry=c), dt)
 
 
-@pytest.mark.parametrize("dt", ["i8", "f32", "i32"])
+@pytest.mark.parametrize("dt", ["i8", "f32", "i32", "f16"])
 def test_sharded_emulation(cuda, oracle, inputs_mod, dt):
     """The multi-GPU Reduce-Scan-Scan path on one GPU: the array is split into
     G contiguous shards; per shard scan_total, an emulated all-gather
@@ -265,20 +265,26 @@ def test_sharded_emulation(cuda, oracle, inputs_mod, dt):
     xd = to_dev(x, dt)
     exclusive = dt == "i8"
     shards = [xd[slice(*shard_bounds(n, G, r))] for r in range(G)]
-    totals_all = torch.cat([cuda.total(s) for s in shards])
+    wss = [cuda.shard_workspace(s) for s in shards]  # one per "rank"
+    totals_all = torch.cat([cuda.shard_reduce(s, ws=w) for s, w in zip(shards, wss)])
+    ref_tot = torch.cat([cuda.total(s) for s in shards])
+    if dt in ("i32", "i8"):
+        assert torch.equal(totals_all, ref_tot)
+    else:
+        assert torch.allclose(totals_all, ref_tot, rtol=1e-12, atol=1e-9)
     outs = []
     for r, s in enumerate(shards):
         y, totals, carry = rss_scan(
             s, exclusive, r, G,
-            local_total=cuda.total,
+            local_total=lambda xl: totals_all[r:r + 1],
             all_gather=lambda t: totals_all,
             carry_of=lambda totals, rr: cuda.carry_from_totals(totals, rr, s.dtype),
-            local_scan=lambda xl, exc, c: (cuda.exclusive if exc else cuda.inclusive)(xl, carry_in=c))
+            local_scan=lambda xl, exc, c: cuda.shard_scan(xl, exc, carry_in=c, ws=wss[r]))
         outs.append(y)
     got = torch.cat(outs)
     torch.cuda.synchronize()
     assert_parity(oracle, got, oracle_1d(oracle, x, dt, exclusive), dt)
-    if dt != "f32":
+    if dt in ("i32", "i8"):  # integers are unique: bit-exact against the single-GPU scan
         whole = (cuda.exclusive if exclusive else cuda.inclusive)(xd)
         assert torch.equal(got, whole)
 
@@ -316,3 +322,27 @@ def test_host_streaming(cuda, oracle, inputs_mod, dt):
         got = cuda.host_scan(h, exclusive=exc, chunk=chunk)
         torch.cuda.synchronize()
         assert_parity(oracle, got, oracle_1d(oracle, x, dt, exc), dt)
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_shard_two_pass(cuda, oracle, inputs_mod, dt, exclusive):
+    """scan_shard_reduce + scan_shard_scan (block rows of 131,072 + ragged tail,
+    carry-in, unaligned fallback) == the oracle with the same carry."""
+    carry_val = {"i32": 123456789, "i8": -77, "f32": 3.25, "f16": -1.5}[dt]
+    cdt = torch.int64 if dt in ("i32", "i8") else torch.float64
+    for n in (131072, 3 * 131072, 5 * 131072 + 777, 40000):
+        x = host_input(inputs_mod, dt, n + 1, seed=n)
+        for off in (0, 1):
+            xs = np.ascontiguousarray(x[off:off + n])
+            xd = to_dev(x, dt)[off:off + n]
+            ws = cuda.shard_workspace(xd)
+            tot = cuda.shard_reduce(xd, ws=ws)
+            ref_tot = oracle.total(xs, dt)
+            if dt in ("i32", "i8"):
+                assert int(tot.item()) == ref_tot
+            else:
+                assert abs(float(tot.item()) - ref_tot) <= 1e-9 * max(1.0, abs(ref_tot))
+            c = torch.tensor([carry_val], dtype=cdt, device="cuda")
+            got = cuda.shard_scan(xd, exclusive, carry_in=c, ws=ws)
+            assert_parity(oracle, got, oracle_1d(oracle, xs, dt, exclusive, carry=carry_val), dt)
