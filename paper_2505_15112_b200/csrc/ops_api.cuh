@@ -5,12 +5,14 @@
 #include "../../include/scan_ops.h"
 #include "sample.cuh"
 #include "split.cuh"
+#include "radix.cuh"
 
 namespace {
 
 using scan::split::SplitParams;
 using scan::split::kThreads;
 using scan::split::kTile;
+using scan::radix::DigitParams;
 
 constexpr size_t kSplitHdr = 128;              // split header inside the scan header block
 constexpr size_t kSplitArrays = kWsDescOffset;  // counts[ntiles] then offs[ntiles]
@@ -109,6 +111,72 @@ void split_ws_setup(SplitParams& p, void* ws, int64_t n)
     p.ntiles = (int)split_tiles(n);
 }
 
+// LSB radix sort with 8-bit digits (radix.cuh): per pass count -> scan of the
+// digit-major counts (this library's exclusive scan) -> stable scatter.
+template <int KT, int ES>
+int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, int descending, uint8_t* w,
+                void* tmp_keys, int32_t* tmp_idx, cudaStream_t s, const DevInfo& di)
+{
+    using namespace scan::radix;
+    auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const int64_t nt = (n + kTile - 1) / kTile;
+    const int64_t nc = nt * kDigits;
+    const size_t scan_ws = up(scan_rows_workspace_bytes(SCAN_I32_I32, kDigits, nt));
+    uint32_t* counts = reinterpret_cast<uint32_t*>(w + scan_ws);
+    uint32_t* offs = reinterpret_cast<uint32_t*>(w + scan_ws + up((size_t)nc * 4));
+    uint32_t* dbase = reinterpret_cast<uint32_t*>(w + scan_ws + 2 * up((size_t)nc * 4));
+    const size_t smem = (size_t)kTile * (ES + 4);
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    static int occ = 1;
+    std::call_once(once, [smem] {
+        err = cudaFuncSetAttribute(k_digit_scatter<KT, ES, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(k_digit_scatter<KT, ES, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+        if (err == cudaSuccess &&
+            (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_digit_scatter<KT, ES, true>, kThreads, smem) !=
+                 cudaSuccess ||
+             occ < 1))
+            occ = 1;
+    });
+    if (err != cudaSuccess) return SCAN_ERR_CUDA;
+    const int passes = ES * 8 / 8;  // 8-bit digits: 2 for 16-bit keys, 4 for 32-bit keys (even)
+    DigitParams p;
+    memset(&p, 0, sizeof(p));
+    p.counts = counts;
+    p.offs = offs;
+    p.dbase = dbase;
+    p.n = n;
+    p.ntiles = (int)nt;
+    p.descending = descending != 0;
+    const int64_t g_count = (int64_t)di.sms * 4 < nt ? (int64_t)di.sms * 4 : nt;
+    const int64_t g_scat = (int64_t)di.sms * occ < nt ? (int64_t)di.sms * occ : nt;
+    const void* src_k = keys;
+    const int32_t* src_i = nullptr;
+    for (int ps = 0; ps < passes; ++ps) {
+        p.keys_in = src_k;
+        p.idx_in = src_i;
+        p.keys_out = (ps & 1) ? keys_out : tmp_keys;
+        p.idx_out = (ps & 1) ? idx_out : tmp_idx;
+        p.shift = 8 * ps;
+        k_digit_count<KT, ES><<<(unsigned)g_count, kThreads, 0, s>>>(p);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        // per digit, the exclusive scan of its tile counts: 256 rows of ntiles (P437 row scan)
+        int st = scan_rows(counts, offs, kDigits, nt, nt, nt, SCAN_I32_I32, 1, w, scan_ws, s);
+        if (st != SCAN_OK) return st;
+        if (src_i)
+            k_digit_scatter<KT, ES, true><<<(unsigned)g_scat, kThreads, smem, s>>>(p);
+        else
+            k_digit_scatter<KT, ES, false><<<(unsigned)g_scat, kThreads, smem, s>>>(p);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        if (cudaGetLastError() != cudaSuccess) return SCAN_ERR_CUDA;
+        src_k = p.keys_out;
+        src_i = p.idx_out;
+    }
+    return SCAN_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -154,12 +222,23 @@ int scan_split(const void* x, const int8_t* flags, void* z, int32_t* idx_out, in
     }
 }
 
+// 8-bit-digit sort workspace: [scan ws of the 256*ntiles counts][counts][offs]
+size_t digit_ws_bytes(int64_t n)
+{
+    auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const int64_t nt = (n + scan::radix::kTile - 1) / scan::radix::kTile;
+    const int64_t nc = nt * scan::radix::kDigits;
+    return up(scan_rows_workspace_bytes(SCAN_I32_I32, scan::radix::kDigits, nt > 0 ? nt : 1)) + 2 * up((size_t)nc * 4) +
+           up(scan::radix::kDigits * 4);
+}
+
 size_t scan_radix_sort_workspace_bytes(int64_t n, int key_type)
 {
     if (n < 0 || key_type < SCAN_KEY_U16 || key_type > SCAN_KEY_F32) return 0;
     const size_t es = key_type <= SCAN_KEY_F16 ? 2 : 4;
     auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    return up(split_ws_bytes(n)) + up((size_t)n * es) + up((size_t)n * 4);
+    const size_t a = up(split_ws_bytes(n)), b = up(digit_ws_bytes(n));
+    return (a > b ? a : b) + up((size_t)n * es) + up((size_t)n * 4);
 }
 
 int scan_radix_sort(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, int key_type, int descending,
@@ -178,8 +257,19 @@ int scan_radix_sort(const void* keys, void* keys_out, int32_t* idx_out, int64_t 
     cudaStream_t s = (cudaStream_t)stream;
     auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
     uint8_t* w = (uint8_t*)ws;
-    void* tmp_keys = w + up(split_ws_bytes(n));
-    int32_t* tmp_idx = reinterpret_cast<int32_t*>(w + up(split_ws_bytes(n)) + up((size_t)n * es));
+    const size_t head = up(split_ws_bytes(n)) > up(digit_ws_bytes(n)) ? up(split_ws_bytes(n)) : up(digit_ws_bytes(n));
+    void* tmp_keys = w + head;
+    int32_t* tmp_idx = reinterpret_cast<int32_t*>(w + head + up((size_t)n * es));
+    if (env_int("SCAN_SORT_BITS", 8) != 1) {
+        switch (key_type) {
+        case SCAN_KEY_U16: return sort_digits<scan::split::KEY_U16, 2>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di);
+        case SCAN_KEY_I16: return sort_digits<scan::split::KEY_I16, 2>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di);
+        case SCAN_KEY_F16: return sort_digits<scan::split::KEY_F16, 2>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di);
+        case SCAN_KEY_U32: return sort_digits<scan::split::KEY_U32, 4>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di);
+        case SCAN_KEY_I32: return sort_digits<scan::split::KEY_I32, 4>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di);
+        default: return sort_digits<scan::split::KEY_F32, 4>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di);
+        }
+    }
     const int bits = es * 8;  // even: pass 0 writes tmp, the last pass writes keys_out
     SplitParams p;
     memset(&p, 0, sizeof(p));

@@ -1,0 +1,253 @@
+// radix.cuh -- LSB radix sort with 8-bit digits: the B200-idiomatic
+// multi-bit variant of the paper's radix sort by 1-bit splits (Sec. 5.3,
+// P286-287).  A 1-bit split is a 2-way stable partition
+// whose offsets are an exclusive scan of the mask; an 8-bit digit pass is the
+// 256-way stable partition whose offsets are the exclusive scan of the
+// per-(digit, tile) counts in digit-major order -- the same scan, over 256
+// counters per tile instead of one.  16-bit keys take 2 passes, 32-bit keys 4
+// (instead of 16 / 32 splits).
+//
+// Per pass:
+//   k_digit_count    counts[d * ntiles + t] = #elements of tile t with digit d
+//                    (warp-private shared-memory histograms);
+//   scan_exclusive   over the 256 * ntiles counts (this library's scan, int32)
+//                    -> offs[d * ntiles + t], the global start of (d, t);
+//   k_digit_scatter  stable rank of every element among the same digit inside
+//                    its tile (warp rounds of 32 consecutive elements,
+//                    __match_any_sync peer groups, warp-private running
+//                    histograms, then a CTA prefix over warps and digits),
+//                    the tile staged in shared memory in (digit, rank) order
+//                    and written out as per-digit runs:
+//                    dest = offs[d][t] + rank_in_tile(d).
+// The key code is P287's order-preserving encoding (floats: MSB flipped when
+// positive, every bit when negative; signed ints: sign bit flipped); keys move
+// unchanged.  Stable; descending uses digit' = 255 - digit.
+#pragma once
+#include <stdint.h>
+
+#include "ptx.cuh"
+#include "split.cuh"  // key_code2, KEY_* enums
+
+namespace scan {
+namespace radix {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kRounds = 16;                       // rounds of 32 elements per warp
+constexpr int kTile = kThreads * kRounds;         // 8192 elements per tile
+constexpr int kDigits = 256;
+
+struct DigitParams {
+    const void* keys_in;
+    void* keys_out;
+    const int32_t* idx_in;   // nullable: the identity permutation
+    int32_t* idx_out;
+    uint32_t* counts;        // [256 * ntiles], digit-major
+    const uint32_t* offs;    // [256 * ntiles], per digit: exclusive scan of its tile counts (row scans)
+    const uint32_t* dbase;   // [256] exclusive scan of the digit totals
+    int64_t n;
+    int ntiles;
+    int shift;               // digit = (code >> shift) & 0xff
+    int descending;
+};
+
+template <int KT, int ES>
+__device__ __forceinline__ uint32_t load_key(const void* base, int64_t i)
+{
+    if constexpr (ES == 2) return __ldg(reinterpret_cast<const uint16_t*>(base) + i);
+    else return __ldg(reinterpret_cast<const uint32_t*>(base) + i);
+}
+
+template <int KT>
+__device__ __forceinline__ uint32_t digit_of(uint32_t key, int shift, int descending)
+{
+    const uint32_t d = (split::key_code2<KT>(key) >> shift) & 0xffu;
+    return descending ? 255u - d : d;
+}
+
+// ---- counts per (digit, tile) --------------------------------------------------
+template <int KT, int ES>
+__global__ void __launch_bounds__(kThreads) k_digit_count(const DigitParams p)
+{
+    __shared__ uint32_t s_hist[kWarps][kDigits];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        for (int i = tid; i < kWarps * kDigits; i += kThreads) (&s_hist[0][0])[i] = 0;
+        __syncthreads();
+        const int64_t t0 = (int64_t)t * kTile + warp * (kRounds * 32);
+        uint32_t key[kRounds];
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            const int64_t e = t0 + r * 32 + lane;
+            key[r] = e < p.n ? load_key<KT, ES>(p.keys_in, e) : 0u;
+        }
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            const int64_t e = t0 + r * 32 + lane;
+            if (e < p.n) atomicAdd(&s_hist[warp][digit_of<KT>(key[r], p.shift, p.descending)], 1u);
+        }
+        __syncthreads();
+        for (int d = tid; d < kDigits; d += kThreads) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) c += s_hist[w][d];
+            p.counts[(int64_t)d * p.ntiles + t] = c;
+        }
+        __syncthreads();
+    }
+}
+
+// ---- stable 256-way partition of every tile to the scanned offsets ---------------
+template <int KT, int ES, bool IDX_IN>
+__global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
+{
+    using K = typename std::conditional<ES == 2, uint16_t, uint32_t>::type;
+    __shared__ uint32_t s_hist[kWarps][kDigits];   // per-warp running counts, then prefix over warps
+    __shared__ uint32_t s_tdp[kDigits];            // tile-local start of digit d
+    __shared__ int64_t s_gb[kDigits];              // global start of digit d minus s_tdp[d]
+    __shared__ uint32_t s_wsum[kWarps];
+    extern __shared__ __align__(16) uint8_t s_dyn[];
+    K* const st_key = reinterpret_cast<K*>(s_dyn);
+    int32_t* const st_idx = reinterpret_cast<int32_t*>(s_dyn + kTile * sizeof(K));
+
+    __shared__ uint32_t s_dbase[kDigits];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    // digit bases: exclusive scan over d of the digit totals (last row-scan
+    // entry + last tile count of every digit)
+    if (tid < kDigits) {
+        const int64_t last = (int64_t)tid * p.ntiles + p.ntiles - 1;
+        const uint32_t tot = p.offs[last] + p.counts[last];
+        uint32_t incl = tot;
+#pragma unroll
+        for (int k = 1; k < 32; k <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, k);
+            if (lane >= k) incl += y;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        s_dbase[tid] = incl - tot;
+    }
+    __syncthreads();
+    if (tid < kDigits) {
+        uint32_t off = 0;
+        for (int w = 0; w < warp; ++w) off += s_wsum[w];
+        s_dbase[tid] += off;
+    }
+    __syncthreads();
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const int64_t t0 = (int64_t)t * kTile;
+        const int64_t rem = p.n - t0;
+        const int mt = rem > kTile ? kTile : (int)rem;
+        for (int i = tid; i < kWarps * kDigits; i += kThreads) (&s_hist[0][0])[i] = 0;
+        __syncthreads();
+
+        // 1. warp rounds: rank among equal digits, in element order
+        const int64_t w0 = t0 + warp * (kRounds * 32);
+        // ES == 2: key | rank << 16 in one register; ES == 4: key and rank apart
+        uint32_t key[kRounds], rank[ES == 2 ? 1 : kRounds];
+        int32_t ix[IDX_IN ? kRounds : 1];
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            const int64_t e = w0 + r * 32 + lane;
+            const bool ok = e < p.n;
+            key[r] = ok ? load_key<KT, ES>(p.keys_in, e) : 0u;
+            if constexpr (IDX_IN) ix[r] = ok ? __ldg(p.idx_in + e) : 0;
+        }
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            const int64_t e = w0 + r * 32 + lane;
+            const bool ok = e < p.n;
+            const uint32_t d = ok ? digit_of<KT>(key[r], p.shift, p.descending) : 256u + lane;  // unique dummy
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const uint32_t before = __popc(peers & lt_mask);
+            uint32_t base = 0;
+            if (ok) base = s_hist[warp][d];
+            if constexpr (ES == 2) key[r] |= (base + before) << 16;
+            else rank[r] = base + before;
+            __syncwarp();
+            if (ok && before == 0) s_hist[warp][d] = base + __popc(peers);  // group leader
+            __syncwarp();
+        }
+        __syncthreads();
+
+        // 2. prefix over warps per digit, tile counts, exclusive scan over digits
+        if (tid < kDigits) {
+            uint32_t run = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t c = s_hist[w][tid];
+                s_hist[w][tid] = run;
+                run += c;
+            }
+            // block-level exclusive scan of run (the tile's digit counts) over 256 digits
+            uint32_t incl = run;
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, dd);
+                if (lane >= dd) incl += y;
+            }
+            if (lane == 31) s_wsum[warp] = incl;
+            s_tdp[tid] = incl - run;  // within-warp exclusive, warp offset added below
+        }
+        __syncthreads();
+        if (tid < kDigits) {
+            uint32_t off = 0;
+            for (int w = 0; w < warp; ++w) off += s_wsum[w];
+            const uint32_t tdp = s_tdp[tid] + off;
+            s_tdp[tid] = tdp;
+            s_gb[tid] = (int64_t)s_dbase[tid] + (int64_t)p.offs[(int64_t)tid * p.ntiles + t] - (int64_t)tdp;
+        }
+        __syncthreads();
+
+        // 3. stage in (digit, rank) order
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            const int64_t e = w0 + r * 32 + lane;
+            if (e < p.n) {
+                const uint32_t k = ES == 2 ? (key[r] & 0xffffu) : key[r];
+                const uint32_t rk = ES == 2 ? (key[r] >> 16) : rank[ES == 2 ? 0 : r];
+                const uint32_t d = digit_of<KT>(k, p.shift, p.descending);
+                const uint32_t s = s_tdp[d] + s_hist[warp][d] + rk;
+                st_key[s] = (K)k;
+                if constexpr (IDX_IN) st_idx[s] = ix[r];
+                else st_idx[s] = (int32_t)e;
+            }
+        }
+        __syncthreads();
+
+        // 4. write out: consecutive staging slots of one digit are consecutive in global memory
+        K* const ko = reinterpret_cast<K*>(p.keys_out);
+        for (int s = tid; s < mt; s += kThreads) {
+            const uint32_t k = st_key[s];
+            const int64_t dest = s_gb[digit_of<KT>(k, p.shift, p.descending)] + s;
+            ko[dest] = (K)k;
+            p.idx_out[dest] = st_idx[s];
+        }
+        __syncthreads();
+    }
+}
+
+// dbase[d] = sum over digits d' < d of the digit totals; the total of digit d
+// is its last row-scan entry plus its last tile count.
+__global__ void __launch_bounds__(kDigits) k_digit_base(const uint32_t* counts, const uint32_t* offs, int ntiles,
+                                                        uint32_t* dbase)
+{
+    __shared__ uint32_t s_w[kDigits / 32];
+    const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
+    const int64_t last = (int64_t)d * ntiles + ntiles - 1;
+    const uint32_t tot = offs[last] + counts[last];
+    uint32_t incl = tot;
+#pragma unroll
+    for (int k = 1; k < 32; k <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, k);
+        if (lane >= k) incl += y;
+    }
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int w = 0; w < warp; ++w) off += s_w[w];
+    dbase[d] = off + incl - tot;
+}
+
+}  // namespace radix
+}  // namespace scan
