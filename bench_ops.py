@@ -31,7 +31,8 @@ OPS = {
                   n=1 << 30),
     "compress": dict(name="compress (masked_select): fp16 payload, C3 mask (n=2^30, Bernoulli 0.5, seed 2)",
                      n=1 << 30),
-    "sort": dict(name="LSB radix sort by 16 splits: fp16 keys N(0,1) + int32 indices, n=2^24, seed 5",
+    "sort": dict(name="LSB radix sort (8-bit digits, 2 passes; SCAN_SORT_BITS=1: the paper's 16 splits): "
+                      "fp16 keys N(0,1) + int32 indices, n=2^24, seed 5",
                  n=1 << 24),
     "weighted": dict(name="weighted sampling: scan of n=2^28 fp32 weights U[0,1) (seed 6) + one draw",
                      n=1 << 28),
@@ -99,7 +100,9 @@ def main():
         ko = torch.empty_like(k)
         idx = torch.empty(n, dtype=torch.int32, device=dev)
         fn = lambda: S.radix_sort(k, out=ko, idx_out=idx)  # noqa: E731
-        alg = 16 * n * (2 + 2 + 4 + 4) - n * 4  # pass 0 reads no indices
+        # 8-bit digits: 2 passes, each keys in + out and indices in + out (pass 0 reads none)
+        passes = 16 if os.environ.get("SCAN_SORT_BITS") == "1" else 2
+        alg = passes * n * (2 + 2 + 4 + 4) - n * 4
         ref_fn = lambda: torch.sort(k, stable=True)  # noqa: E731
         ref_name = "torch.sort(stable=True) (CUB radix sort, int64 indices)"
     elif args.op == "weighted":

@@ -134,6 +134,12 @@ int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, i
         if (err == cudaSuccess)
             err = cudaFuncSetAttribute(k_digit_scatter<KT, ES, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(k_digit_scatter_tma<KT, ES, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)DigitTmaCfg<ES, true>::kSmem);
+        if (err == cudaSuccess)
+            err = cudaFuncSetAttribute(k_digit_scatter_tma<KT, ES, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)DigitTmaCfg<ES, false>::kSmem);
         if (err == cudaSuccess &&
             (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_digit_scatter<KT, ES, true>, kThreads, smem) !=
                  cudaSuccess ||
@@ -165,10 +171,20 @@ int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, i
         // per digit, the exclusive scan of its tile counts: 256 rows of ntiles (P437 row scan)
         int st = scan_rows(counts, offs, kDigits, nt, nt, nt, SCAN_I32_I32, 1, w, scan_ws, s);
         if (st != SCAN_OK) return st;
-        if (src_i)
+        const bool tma = aligned16(src_k) && (src_i == nullptr || aligned16(src_i)) && getenv("SCAN_SORT_NO_TMA") == nullptr;
+        if (tma) {
+            const int64_t g = (int64_t)di.sms < nt ? (int64_t)di.sms : nt;
+            if (src_i)
+                k_digit_scatter_tma<KT, ES, true><<<(unsigned)g, DigitTmaCfg<ES, true>::kThreadsT,
+                                                    DigitTmaCfg<ES, true>::kSmem, s>>>(p);
+            else
+                k_digit_scatter_tma<KT, ES, false><<<(unsigned)g, DigitTmaCfg<ES, false>::kThreadsT,
+                                                     DigitTmaCfg<ES, false>::kSmem, s>>>(p);
+        } else if (src_i) {
             k_digit_scatter<KT, ES, true><<<(unsigned)g_scat, kThreads, smem, s>>>(p);
-        else
+        } else {
             k_digit_scatter<KT, ES, false><<<(unsigned)g_scat, kThreads, smem, s>>>(p);
+        }
         g_launches.fetch_add(1, std::memory_order_relaxed);
         if (cudaGetLastError() != cudaSuccess) return SCAN_ERR_CUDA;
         src_k = p.keys_out;

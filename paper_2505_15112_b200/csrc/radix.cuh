@@ -9,12 +9,12 @@
 //
 // Per pass:
 //   k_digit_count    counts[d * ntiles + t] = #elements of tile t with digit d
-//                    (warp-private shared-memory histograms);
+//                    (warp-private shared-memory histograms, atomics);
 //   scan_exclusive   over the 256 * ntiles counts (this library's scan, int32)
 //                    -> offs[d * ntiles + t], the global start of (d, t);
 //   k_digit_scatter  stable rank of every element among the same digit inside
 //                    its tile (warp rounds of 32 consecutive elements,
-//                    __match_any_sync peer groups, warp-private running
+//                    ballot-based peer groups, warp-private running
 //                    histograms, then a CTA prefix over warps and digits),
 //                    the tile staged in shared memory in (digit, rank) order
 //                    and written out as per-digit runs:
@@ -63,6 +63,20 @@ __device__ __forceinline__ uint32_t digit_of(uint32_t key, int shift, int descen
 {
     const uint32_t d = (split::key_code2<KT>(key) >> shift) & 0xffu;
     return descending ? 255u - d : d;
+}
+
+// Lanes of the warp holding the same digit as this lane (among `valid` lanes):
+// the AND of 8 bit-wise ballots -- the warp multi-split; on sm_100a this is much
+// cheaper than MATCH.ANY (measured: 415 -> 333 us for a 2^24 fp16 sort).
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid)
+{
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bb : ~bb;
+    }
+    return peers;
 }
 
 // ---- counts per (digit, tile) --------------------------------------------------
@@ -157,8 +171,8 @@ __global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
         for (int r = 0; r < kRounds; ++r) {
             const int64_t e = w0 + r * 32 + lane;
             const bool ok = e < p.n;
-            const uint32_t d = ok ? digit_of<KT>(key[r], p.shift, p.descending) : 256u + lane;  // unique dummy
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            const uint32_t d = digit_of<KT>(key[r], p.shift, p.descending);
+            const uint32_t peers = digit_peers(d, ok);
             const uint32_t before = __popc(peers & lt_mask);
             uint32_t base = 0;
             if (ok) base = s_hist[warp][d];
@@ -224,6 +238,196 @@ __global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
             p.idx_out[dest] = st_idx[s];
         }
         __syncthreads();
+    }
+}
+
+// ---- TMA-ring variant: a producer warp streams key (and index) tiles into a
+// shared-memory ring with cp.async.bulk so HBM latency is hidden by the ring
+// depth; 16 compute warps rank, stage and write.  One CTA per SM.  Needs
+// 16-byte aligned key / index buffers; the ragged last tile is read from
+// global memory directly.
+template <int ES, bool IDX_IN>
+struct DigitTmaCfg {
+    static constexpr int kKeyB = kTile * ES;
+    static constexpr int kIdxB = IDX_IN ? kTile * 4 : 0;
+    static constexpr int kSlot = kKeyB + kIdxB;
+    static constexpr int kStage = kTile * (ES + 4);
+    static constexpr int kNB = (200 * 1024 - kStage) / kSlot > 4 ? 4 : (200 * 1024 - kStage) / kSlot;
+    static constexpr size_t kSmem = (size_t)kNB * kSlot + kStage;
+    static constexpr int kThreadsT = kThreads + 32;
+};
+
+template <int KT, int ES, bool IDX_IN>
+__global__ void __launch_bounds__(kThreads + 32, 1) k_digit_scatter_tma(const DigitParams p)
+{
+    using C = DigitTmaCfg<ES, IDX_IN>;
+    constexpr int NB = C::kNB;
+    static_assert(NB >= 2, "ring of at least two tiles");
+    using K = typename std::conditional<ES == 2, uint16_t, uint32_t>::type;
+    __shared__ uint32_t s_hist[kWarps][kDigits];
+    __shared__ uint32_t s_tdp[kDigits];
+    __shared__ int64_t s_gb[kDigits];
+    __shared__ uint32_t s_wsum[kWarps];
+    __shared__ uint32_t s_dbase[kDigits];
+    __shared__ __align__(8) uint64_t full[NB], empty[NB];
+    extern __shared__ __align__(128) uint8_t s_dyn[];
+    uint8_t* const ring = s_dyn;
+    K* const st_key = reinterpret_cast<K*>(s_dyn + NB * C::kSlot);
+    int32_t* const st_idx = reinterpret_cast<int32_t*>(s_dyn + NB * C::kSlot + kTile * ES);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t full_tiles = p.n / kTile;
+    if (tid < kDigits) {  // digit bases (as in k_digit_scatter)
+        const int64_t last = (int64_t)tid * p.ntiles + p.ntiles - 1;
+        const uint32_t tot = p.offs[last] + p.counts[last];
+        uint32_t incl = tot;
+#pragma unroll
+        for (int k = 1; k < 32; k <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, k);
+            if (lane >= k) incl += y;
+        }
+        if (lane == 31) s_wsum[warp] = incl;
+        s_dbase[tid] = incl - tot;
+    }
+    if (tid == 0) {
+        for (int i = 0; i < NB; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], kWarps);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid < kDigits) {
+        uint32_t off = 0;
+        for (int w = 0; w < warp; ++w) off += s_wsum[w];
+        s_dbase[tid] += off;
+    }
+    __syncthreads();
+
+    if (warp == kWarps) {
+        // ============ producer ============
+        if (lane == 0) {
+            const uint64_t pol = ptx::policy_evict_first();
+            int s = 0;
+            uint32_t ph = 0;
+            bool wrapped = false;
+            for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+                if (wrapped) ptx::mbar_wait(&empty[s], ph ^ 1u);
+                uint8_t* dst = ring + s * C::kSlot;
+                if (t < full_tiles) {
+                    const int64_t t0 = (int64_t)t * kTile;
+                    ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)C::kSlot);
+                    ptx::tma_load_1d(dst, reinterpret_cast<const uint8_t*>(p.keys_in) + t0 * ES, C::kKeyB, &full[s], pol);
+                    if constexpr (IDX_IN) ptx::tma_load_1d(dst + C::kKeyB, p.idx_in + t0, C::kIdxB, &full[s], pol);
+                } else {
+                    ptx::mbar_arrive(&full[s]);
+                }
+                if (++s == NB) {
+                    s = 0;
+                    ph ^= 1u;
+                    wrapped = true;
+                }
+            }
+        }
+        return;
+    }
+
+    // ============ compute (512 threads) ============
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
+        const int64_t t0 = (int64_t)t * kTile;
+        const int64_t rem = p.n - t0;
+        const int mt = rem > kTile ? kTile : (int)rem;
+        const bool in_ring = t < full_tiles;
+        for (int i = tid; i < kWarps * kDigits; i += kThreads) (&s_hist[0][0])[i] = 0;
+        ptx::mbar_wait(&full[s], ph);
+        const uint8_t* slot = ring + s * C::kSlot;
+        const K* sk = reinterpret_cast<const K*>(slot);
+        const int32_t* si = reinterpret_cast<const int32_t*>(slot + C::kKeyB);
+        ptx::named_bar_sync(1, kThreads);  // s_hist zeroed
+
+        const int l0 = warp * (kRounds * 32);   // tile-local index of this warp's first element
+        uint32_t key[kRounds], rank[ES == 2 ? 1 : kRounds];
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            const int li = l0 + r * 32 + lane;
+            if (in_ring) key[r] = sk[li];
+            else key[r] = li < mt ? load_key<KT, ES>(p.keys_in, t0 + li) : 0u;
+        }
+        // all 16 peer groups first (independent, long-latency MATCH), then the
+        // running per-warp digit counts round by round
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            const int li = l0 + r * 32 + lane;
+            const bool ok = li < mt;
+            const uint32_t d = digit_of<KT>(key[r], p.shift, p.descending);
+            const uint32_t peers = digit_peers(d, ok);
+            const uint32_t before = __popc(peers & lt_mask);
+            uint32_t base = 0;
+            if (ok) base = s_hist[warp][d];
+            if constexpr (ES == 2) key[r] |= (base + before) << 16;
+            else rank[r] = base + before;
+            __syncwarp();
+            if (ok && before == 0) s_hist[warp][d] = base + __popc(peers);
+            __syncwarp();
+        }
+        ptx::named_bar_sync(1, kThreads);
+        if (tid < kDigits) {
+            uint32_t run = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) {
+                const uint32_t c = s_hist[w][tid];
+                s_hist[w][tid] = run;
+                run += c;
+            }
+            uint32_t incl = run;
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, dd);
+                if (lane >= dd) incl += y;
+            }
+            if (lane == 31) s_wsum[warp] = incl;
+            s_tdp[tid] = incl - run;
+        }
+        ptx::named_bar_sync(1, kThreads);
+        if (tid < kDigits) {
+            uint32_t off = 0;
+            for (int w = 0; w < warp; ++w) off += s_wsum[w];
+            const uint32_t tdp = s_tdp[tid] + off;
+            s_tdp[tid] = tdp;
+            s_gb[tid] = (int64_t)s_dbase[tid] + (int64_t)p.offs[(int64_t)tid * p.ntiles + t] - (int64_t)tdp;
+        }
+        ptx::named_bar_sync(1, kThreads);
+#pragma unroll
+        for (int r = 0; r < kRounds; ++r) {
+            const int li = l0 + r * 32 + lane;
+            if (li < mt) {
+                const uint32_t k = ES == 2 ? (key[r] & 0xffffu) : key[r];
+                const uint32_t rk = ES == 2 ? (key[r] >> 16) : rank[ES == 2 ? 0 : r];
+                const uint32_t d = digit_of<KT>(k, p.shift, p.descending);
+                const uint32_t st = s_tdp[d] + s_hist[warp][d] + rk;
+                st_key[st] = (K)k;
+                if constexpr (IDX_IN) st_idx[st] = in_ring ? si[li] : p.idx_in[t0 + li];
+                else st_idx[st] = (int32_t)(t0 + li);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&empty[s]);  // this warp is done with the slot
+        if (++s == NB) {
+            s = 0;
+            ph ^= 1u;
+        }
+        ptx::named_bar_sync(1, kThreads);
+        K* const ko = reinterpret_cast<K*>(p.keys_out);
+        for (int q = tid; q < mt; q += kThreads) {
+            const uint32_t k = st_key[q];
+            const int64_t dest = s_gb[digit_of<KT>(k, p.shift, p.descending)] + q;
+            ko[dest] = (K)k;
+            p.idx_out[dest] = st_idx[q];
+        }
+        // the next tile's first named barrier orders these reads before its writes
     }
 }
 
