@@ -104,6 +104,17 @@ SCAN_API int scan_top_p_draw(const float* cdf, const int64_t* order, int64_t row
                              int64_t cdf_row_stride, int64_t order_row_stride, float p, const float* u,
                              int64_t* token_out, int32_t* kept_out, void* stream);
 
+/* Top-p sampling of `rows` rows WITHOUT a full sort (Sec. 5.5, R15): per row
+ * the candidates {q >= tau} (tau lowered until their mass reaches p) are
+ * sorted in shared memory by (probability descending, column ascending) --
+ * the stable descending order -- scanned in fp64, and the nucleus / draw
+ * taken as in scan_top_p_draw.  probs: row r at probs + r*row_stride, fp32,
+ * non-negative; u [rows] uniform draws.  token_out [rows] int64 (-1: the row
+ * needs more than 8192 candidates to reach p -- use the sort path,
+ * scan_top_p_draw), kept_out NULL or [rows] int32 nucleus sizes. */
+SCAN_API int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t row_stride, float p,
+                               const float* u, int64_t* token_out, int32_t* kept_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

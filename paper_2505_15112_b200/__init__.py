@@ -104,6 +104,8 @@ def load() -> ctypes.CDLL:
         L.scan_weighted_sample.restype = I
         L.scan_top_p_draw.argtypes = [P, P, I64, I64, I64, I64, ctypes.c_float, P, P, P, P]
         L.scan_top_p_draw.restype = I
+        L.scan_top_p_sample.argtypes = [P, I64, I64, I64, ctypes.c_float, P, P, P, P]
+        L.scan_top_p_sample.restype = I
         _lib = L
     return _lib
 
@@ -396,23 +398,38 @@ def weighted_sample(w: torch.Tensor, theta: float, cdf=None, stream=None) -> tor
     return out
 
 
-def top_p_sample(probs: torch.Tensor, p: float, u: torch.Tensor, stream=None):
-    """P298-299 top-p (nucleus) sampling of every row of `probs` [rows, cols]:
-    descending sort (torch.sort, a library segmented sort), our row scan
-    (scan_rows, P437) of the sorted probabilities, then our nucleus + inverse
-    transform draw (scan_top_p_draw, R15) with the uniform draws u [rows].
+def top_p_sample(probs: torch.Tensor, p: float, u: torch.Tensor, stream=None, method: str = "select"):
+    """P298-299 top-p (nucleus) sampling of every row of `probs` [rows, cols].
+
+    method="select" (default): no full sort -- per row the candidates
+    {q >= tau} are sorted in shared memory and scanned (scan_top_p_sample);
+    rows that need more than 8192 candidates fall back to the sort path.
+    method="sort": the paper's pipeline -- descending row sort (torch.sort, a
+    library segmented sort), our row scan (scan_rows, P437) of the sorted
+    probabilities, our nucleus + inverse transform draw (scan_top_p_draw, R15).
 
     Returns (tokens int64 [rows], nucleus sizes int32 [rows])."""
     if not (probs.is_cuda and u.is_cuda) or probs.dtype != torch.float32 or u.dtype != torch.float32:
         raise ScanError("probs and u must be CUDA float32 tensors (there is no CPU path)")
-    if probs.dim() != 2 or u.numel() != probs.shape[0]:
-        raise ScanError("probs must be [rows, cols] and u [rows]")
+    if probs.dim() != 2 or u.numel() != probs.shape[0] or (probs.shape[1] > 1 and probs.stride(1) != 1):
+        raise ScanError("probs must be [rows, cols] with unit column stride and u [rows]")
     R, C = probs.shape
-    sp, order = torch.sort(probs, dim=1, descending=True, stable=True)
-    cdf = rows(sp)
+    u = u.contiguous()
     tok = torch.empty(R, dtype=torch.int64, device=probs.device)
     kept = torch.empty(R, dtype=torch.int32, device=probs.device)
+    if method == "select":
+        _check(load().scan_top_p_sample(_ptr(probs), R, C, probs.stride(0) if R > 1 else C, float(p), _ptr(u),
+                                        _ptr(tok), _ptr(kept), _stream_ptr(stream)), "scan_top_p_sample")
+        miss = torch.nonzero(tok < 0).flatten()
+        if miss.numel() == 0:
+            return tok, kept
+        t2, k2 = top_p_sample(probs[miss], p, u[miss], stream=stream, method="sort")
+        tok[miss] = t2
+        kept[miss] = k2
+        return tok, kept
+    sp, order = torch.sort(probs, dim=1, descending=True, stable=True)
+    cdf = rows(sp)
     _check(load().scan_top_p_draw(_ptr(cdf), _ptr(order), R, C, cdf.stride(0), order.stride(0), float(p),
-                                  _ptr(u.contiguous()), _ptr(tok), _ptr(kept), _stream_ptr(stream)),
+                                  _ptr(u), _ptr(tok), _ptr(kept), _stream_ptr(stream)),
            "scan_top_p_draw")
     return tok, kept

@@ -4,6 +4,7 @@
 #pragma once
 #include "../../include/scan_ops.h"
 #include "sample.cuh"
+#include "topp.cuh"
 #include "split.cuh"
 #include "radix.cuh"
 
@@ -342,6 +343,35 @@ int scan_top_p_draw(const float* cdf, const int64_t* order, int64_t rows, int64_
     if (st != SCAN_OK) return st;
     scan::sample::k_top_p_draw<<<(unsigned)rows, scan::sample::kThreads, 0, (cudaStream_t)stream>>>(
         cdf, order, cols, cdf_row_stride, order_row_stride, p, u, token_out, kept_out);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+}
+
+int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t row_stride, float p, const float* u,
+                      int64_t* token_out, int32_t* kept_out, void* stream)
+{
+    if (rows < 0 || cols < 0 || row_stride < cols) return SCAN_ERR_ARG;
+    if (rows == 0) return SCAN_OK;
+    if (cols == 0 || cols >= ((int64_t)1 << 31) || probs == nullptr || u == nullptr || token_out == nullptr)
+        return SCAN_ERR_ARG;
+    DevInfo di;
+    int st = dev_info(di);
+    if (st != SCAN_OK) return st;
+    using namespace scan::topp;
+    const size_t smem = (size_t)kCap * 8;
+    static std::once_flag once;
+    static cudaError_t err = cudaSuccess;
+    static int occ = 1;
+    std::call_once(once, [smem] {
+        err = cudaFuncSetAttribute(k_top_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (err == cudaSuccess &&
+            (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_top_p, scan::topp::kThreads, smem) != cudaSuccess || occ < 1))
+            occ = 1;
+    });
+    if (err != cudaSuccess) return SCAN_ERR_CUDA;
+    const int64_t g = (int64_t)di.sms * occ < rows ? (int64_t)di.sms * occ : rows;
+    k_top_p<<<(unsigned)g, scan::topp::kThreads, smem, (cudaStream_t)stream>>>(probs, rows, cols, row_stride, p, u, token_out,
+                                                                    kept_out);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
 }

@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) k_digit_scatter_tma(const Di
     __shared__ uint32_t s_wsum[kWarps];
     __shared__ uint32_t s_dbase[kDigits];
     __shared__ __align__(8) uint64_t full[NB], empty[NB];
-    extern __shared__ __align__(128) uint8_t s_dyn[];
+    extern __shared__ __align__(16) uint8_t s_dyn[];
     uint8_t* const ring = s_dyn;
     K* const st_key = reinterpret_cast<K*>(s_dyn + NB * C::kSlot);
     int32_t* const st_idx = reinterpret_cast<int32_t*>(s_dyn + NB * C::kSlot + kTile * ES);

@@ -170,7 +170,8 @@ def test_weighted_sample_parity(cuda, oracle, inputs_mod):
         assert same >= len(thetas) - 1  # differs only when t sits within rounding of a boundary
 
 
-def test_top_p_parity(cuda, oracle, inputs_mod):
+@pytest.mark.parametrize("method", ["select", "sort"])
+def test_top_p_parity(cuda, oracle, inputs_mod, method):
     """C4-style rows (softmax(4 z)), several p; token and nucleus size match the
     oracle except where a threshold sits within float rounding of a boundary,
     and are always valid draws within the scan tolerance."""
@@ -181,7 +182,7 @@ def test_top_p_parity(cuda, oracle, inputs_mod):
     u = rng.random(R).astype(np.float32)
     ud = torch.from_numpy(u).cuda()
     for p in (0.0, 0.5, 0.9, 0.95, 2.0):
-        tok, kept = cuda.top_p_sample(Pd, p, ud)
+        tok, kept = cuda.top_p_sample(Pd, p, ud, method=method)
         tok, kept = tok.cpu().numpy(), kept.cpu().numpy()
         agree = 0
         for r in range(R):
@@ -197,3 +198,23 @@ def test_top_p_parity(cuda, oracle, inputs_mod):
             assert rank < K and _valid_interval(C64, rank, float(u[r]) * C64[K - 1], tol)
             agree += (tok[r] == rt) and (K == rk)
         assert agree >= R - 2, (p, agree)
+
+
+def test_top_p_select_edge_rows(cuda, oracle):
+    """Sort-free top-p on hand-made rows: ties across the nucleus boundary
+    (stable index order), a flat row that needs the sort fallback, zeros, a
+    single dominant token, a ragged column count."""
+    C = 50001
+    rows = []
+    r0 = np.zeros(C, np.float32); r0[[5, 17, 900, 40000]] = 0.25; rows.append(r0)     # 4-way tie
+    r1 = np.full(C, 1.0 / C, np.float32); rows.append(r1)                             # flat: fallback
+    r2 = np.zeros(C, np.float32); r2[123] = 1.0; rows.append(r2)                      # one token
+    rng = np.random.default_rng(4)
+    r3 = rng.random(C).astype(np.float32) ** 8; r3 /= r3.sum(); rows.append(r3)
+    P = np.stack(rows)
+    u = np.array([0.1, 0.5, 0.9, 0.77], np.float32)
+    for p in (0.3, 0.6, 0.9):
+        tok, kept = cuda.top_p_sample(torch.from_numpy(P).cuda(), p, torch.from_numpy(u).cuda())
+        for r in range(len(rows)):
+            rt, rk = oracle.top_p_sample(P[r], p, float(u[r]))
+            assert int(tok[r]) == rt and int(kept[r]) == rk, (p, r, int(tok[r]), rt, int(kept[r]), rk)
