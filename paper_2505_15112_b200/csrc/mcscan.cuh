@@ -115,6 +115,7 @@ struct McParams16 {
     int exclusive;
     int debug;
     int ahead;              // reduce jobs run this many chunks ahead of scan jobs (1..2)
+    int l2;                 // L2 policies: bits 0-1 Phase-I read, bits 2-3 Phase-II re-read (0 = default)
 };
 
 template <int DT, int NC, int GPW, int NB_IN, int NB_OUT>
@@ -516,8 +517,20 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     if (warp == 0) {
         // =========================== producer ===========================
         if (lane == 0) {
-            const uint64_t pol_keep = ptx::policy_evict_last();
-            const uint64_t pol_drop = ptx::policy_evict_first();
+            // L2 policy of the Phase-I read (kept for the Phase-II re-read) and
+            // of the re-read (dead afterwards); p.l2 selects alternatives (A/B)
+            uint64_t pol_keep, pol_drop;
+            switch (p.l2 & 3) {
+            case 1: pol_keep = ptx::policy_evict_normal(); break;
+            case 2: pol_keep = ptx::policy_evict_last_frac(0.5f); break;
+            case 3: pol_keep = ptx::policy_evict_unchanged(); break;
+            default: pol_keep = ptx::policy_evict_last(); break;
+            }
+            switch ((p.l2 >> 2) & 3) {
+            case 1: pol_drop = ptx::policy_evict_normal(); break;
+            case 2: pol_drop = ptx::policy_evict_unchanged(); break;
+            default: pol_drop = ptx::policy_evict_first(); break;
+            }
             Ring<NB_IN> rin;
             for (int q = 0; q < njobs; ++q) {
                 int c, t0, t1;

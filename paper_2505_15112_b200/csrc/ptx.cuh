@@ -74,6 +74,28 @@ __device__ __forceinline__ uint64_t policy_evict_last()
     return pol;
 }
 
+__device__ __forceinline__ uint64_t policy_evict_normal()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_unchanged()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// evict_last on `fraction` of the accessed lines, priority unchanged on the rest
+__device__ __forceinline__ uint64_t policy_evict_last_frac(float fraction)
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, %1;" : "=l"(pol) : "f"(fraction));
+    return pol;
+}
+
 // global -> shared, completion signalled on `bar` (complete_tx of `bytes`).
 __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src, uint32_t bytes,
                                             uint64_t* bar, uint64_t policy)
