@@ -61,25 +61,33 @@ int launch_split_t(SplitParams& p, cudaStream_t s, const DevInfo& di)
 }
 
 // TMA-ring scatter (split.cuh k_split_scatter_tma): aligned buffers, ES <= 4.
-template <int SRC, int ES, int KT, bool IDX_IN>
-int launch_split_tma(SplitParams& p, cudaStream_t s, const DevInfo& di)
+template <int SRC, int ES, int KT, bool IDX_IN, bool CMP>
+int launch_split_tma_c(SplitParams& p, cudaStream_t s, const DevInfo& di)
 {
     using namespace scan::split;
     using C = TmaCfg<SRC, ES, IDX_IN>;
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(k_split_scatter_tma<SRC, ES, KT, IDX_IN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)C::kSmem);
+        err = cudaFuncSetAttribute(k_split_scatter_tma<SRC, ES, KT, IDX_IN, CMP>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
     });
     if (err != cudaSuccess) return SCAN_ERR_CUDA;
     const int64_t want_count = ((int64_t)p.ntiles + kWarps - 1) / kWarps;
     const int64_t g_count = (int64_t)di.sms * 4 < want_count ? (int64_t)di.sms * 4 : want_count;
     const int64_t g_scat = (int64_t)di.sms < p.ntiles ? (int64_t)di.sms : p.ntiles;
     k_split_count<SRC, ES, KT><<<(unsigned)g_count, kThreads, 0, s>>>(p);
-    k_split_scatter_tma<SRC, ES, KT, IDX_IN><<<(unsigned)g_scat, C::kThreadsT, C::kSmem, s>>>(p);
+    k_split_scatter_tma<SRC, ES, KT, IDX_IN, CMP><<<(unsigned)g_scat, C::kThreadsT, C::kSmem, s>>>(p);
     g_launches.fetch_add(2, std::memory_order_relaxed);
     return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+}
+
+template <int SRC, int ES, int KT, bool IDX_IN>
+int launch_split_tma(SplitParams& p, cudaStream_t s, const DevInfo& di)
+{
+    if constexpr (SRC == scan::split::SRC_FLAGS && !IDX_IN)
+        if (p.compress) return launch_split_tma_c<SRC, ES, KT, IDX_IN, true>(p, s, di);
+    return launch_split_tma_c<SRC, ES, KT, IDX_IN, false>(p, s, di);
 }
 
 template <int SRC, int ES, int KT>

@@ -466,7 +466,8 @@ struct TmaCfg {
     static constexpr size_t kSmem = (size_t)kNB * kSlot + kStage + 128;
 };
 
-template <int SRC, int ES, int KT, bool IDX_IN>
+// CMP: compress -- only the trues are staged and written.
+template <int SRC, int ES, int KT, bool IDX_IN, bool CMP = false>
 __global__ void __launch_bounds__(TmaCfg<SRC, ES, IDX_IN>::kThreadsT, 1) k_split_scatter_tma(const SplitParams p)
 {
     using C = TmaCfg<SRC, ES, IDX_IN>;
@@ -600,15 +601,16 @@ __global__ void __launch_bounds__(TmaCfg<SRC, ES, IDX_IN>::kThreadsT, 1) k_split
             for (int j = 0; j < kPer; ++j) {
                 if (j >= m) break;
                 const uint32_t below = __popc(bits & ((1u << j) - 1u));  // trues before j in this thread
-                const uint32_t pos = ((bits >> j) & 1u) ? tb + below : fb + (uint32_t)j - below;
+                const bool tr = (bits >> j) & 1u;
+                const uint32_t pos = tr ? tb + below : fb + (uint32_t)j - below;
                 uint32_t pay;
                 if constexpr (ES == 2) pay = (L.w[j >> 1] >> (16 * (j & 1))) & 0xffffu;
                 else pay = (L.w[j >> 2] >> (8 * (j & 3))) & 0xffu;
-                s_pk[pos] = (pay << 16) | (uint32_t)(ct_ * kPer + j);
+                if (!CMP || tr) s_pk[pos] = (pay << 16) | (uint32_t)(ct_ * kPer + j);
             }
             ptx::named_bar_sync(1, kThreads);
             write_run_packed<ES>(zb, p.idx_out, off_t, (int32_t)t0, s_pk, sh_t, (int)ct, ct_);
-            if (!p.compress) write_run_packed<ES>(zb, p.idx_out, fbase, (int32_t)t0, s_pk, fst, mt - (int)ct, ct_);
+            if (!CMP) write_run_packed<ES>(zb, p.idx_out, fbase, (int32_t)t0, s_pk, fst, mt - (int)ct, ct_);
         } else {
             // Staging positions are shifted so that staging index == global index
             // (mod VE): the middle of each run is then written with 16-byte stores.
@@ -628,7 +630,7 @@ __global__ void __launch_bounds__(TmaCfg<SRC, ES, IDX_IN>::kThreadsT, 1) k_split
             }
             ptx::named_bar_sync(1, kThreads);
             write_run<ES>(zb, p.idx_out, off_t, s_stage, s_idx, sh_t, (int)ct, ct_);
-            if (!p.compress) write_run<ES>(zb, p.idx_out, fbase, s_stage, s_idx, fst, mt - (int)ct, ct_);
+            if (!CMP) write_run<ES>(zb, p.idx_out, fbase, s_stage, s_idx, fst, mt - (int)ct, ct_);
         }
         // the next tile's first named barrier orders these staging reads before its writes
     }
