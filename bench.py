@@ -360,6 +360,13 @@ def run_ours(args, rank, world, local_rank):
         cpu = {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
                "sample": f"{sample}; {t:.1f} s of single-thread oracle time on the GPU box host"}
 
+    # ---- same-run ceilings, outside the timed region: the scan's
+    # traffic as a pure stream (widen copy), a D2D memcpy of the same bytes, and
+    # torch.cumsum (CUB) on the same input -- context for roofline.frac
+    ceilings = None
+    if world == 1 and cfg != "C1" and not args.no_ceilings:
+        ceilings = measure_ceilings(x, out, w, stream, local_bytes, kernel_ms)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
@@ -378,11 +385,59 @@ def run_ours(args, rank, world, local_rank):
                 else "hot L2 (latency-bound size)",
                 "cuda_graph": graph is not None,
             },
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "roofline": roof, "ceilings": ceilings, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     return 0
+
+
+def measure_ceilings(x, out, w, stream, nbytes, scan_ms):
+    """GB/s (in+out algorithmic bytes) of streams with the scan's exact traffic."""
+    import torch
+
+    import paper_2505_15112_b200 as S
+
+    def timed(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+    res = {}
+    xf, of = x.reshape(-1), out.reshape(-1)
+    try:
+        ms = timed(lambda: S.widen_copy(xf, of))
+        res["widen_copy_GBps"] = round(nbytes / (ms * 1e-3) / 1e9, 1)
+        res["scan_vs_widen_copy"] = round(ms / scan_ms, 4)
+    except Exception as e:  # noqa: BLE001
+        res["widen_copy_error"] = str(e)[:80]
+    half = nbytes // 2
+    src = xf.view(torch.uint8) if xf.element_size() * xf.numel() >= half else None
+    if src is not None:
+        dst = of.view(torch.uint8)
+        ms = timed(lambda: dst[:half].copy_(src[:half]))
+        res["memcpy_d2d_GBps"] = round(2 * half / (ms * 1e-3) / 1e9, 1)
+    if x.numel() >= (1 << 31):
+        res["torch_cumsum_GBps"] = None
+        res["torch_cumsum_note"] = "not run: torch.cumsum faults (illegal address) beyond 2^31 elements on this build"
+        res["note"] = "same run, outside the timed region; widen_copy = libscan's 16-byte stream of the scan's exact bytes"
+        return res
+    try:
+        odt = torch.int32 if w["dt"] in ("i32", "i8") else torch.float32
+        if w["rows"] > 1:
+            ms = timed(lambda: torch.cumsum(x, dim=1, dtype=odt, out=out), reps=2)
+        else:
+            ms = timed(lambda: torch.cumsum(xf, dim=0, dtype=odt, out=of), reps=2)
+        res["torch_cumsum_GBps"] = round(nbytes / (ms * 1e-3) / 1e9, 1)
+    except Exception as e:  # noqa: BLE001
+        res["torch_cumsum_error"] = str(e)[:80]
+    res["note"] = "same run, outside the timed region; widen_copy = libscan's 16-byte stream of the scan's exact bytes"
+    return res
 
 
 def run_e2e(args, x, out, out2, scan_call, dev, stream, world, barrier, local_elems, w, step_bytes):
@@ -444,6 +499,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(WORK), default="C5")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ceilings", action="store_true", help="skip the same-run widen-copy / memcpy / cumsum ceilings")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunk", type=int, default=1 << 26, help="elements per host-streaming chunk")
     ap.add_argument("--no-cpu-baseline", action="store_true")

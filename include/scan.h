@@ -161,6 +161,13 @@ SCAN_API int scan_shard_reduce(const void* in, int64_t n, int dtype, void* total
 SCAN_API int scan_shard_scan(const void* in, void* out, int64_t n, int dtype, int exclusive, const void* carry_in,
                              void* ws, size_t ws_bytes, void* stream);
 
+/* Measurement ceiling (not a scan): out[i] = widen(in[i]) for n elements --
+ * exactly the HBM traffic of a scan of the same dtype with no scan arithmetic
+ * (a 16-byte streaming copy).  bench.py times it in the same run as the scan
+ * (SURVEY 8(d) "matched-traffic widen-copy").  16-byte aligned buffers only
+ * (SCAN_ERR_ARG otherwise). */
+SCAN_API int scan_widen_copy(const void* in, void* out, int64_t n, int dtype, void* stream);
+
 /* End-to-end scan of an array in HOST memory (pinned for full speed): the
  * array is streamed through the GPU in chunks of `chunk_elems` elements with
  * the host->device copy of chunk i+1, the scan of chunk i and the

@@ -85,6 +85,8 @@ def load() -> ctypes.CDLL:
         L.scan_host_stage_bytes.restype = SZ
         L.scan_host.argtypes = [P, P, I64, I, I, I64, P, SZ, P, SZ, P]
         L.scan_host.restype = I
+        L.scan_widen_copy.argtypes = [P, P, I64, I, P]
+        L.scan_widen_copy.restype = I
         L.scan_shard_workspace_bytes.argtypes = [I, I64]
         L.scan_shard_workspace_bytes.restype = SZ
         L.scan_shard_reduce.argtypes = [P, I64, I, P, P, SZ, P]
@@ -309,6 +311,13 @@ def shard_scan(x: torch.Tensor, exclusive: bool = False, carry_in=None, ws: Work
     ws = ws if ws is not None else workspace(L.scan_shard_workspace_bytes(dt, n), x.device, stream)
     _check(L.scan_shard_scan(_ptr(x), _ptr(out), n, dt, int(bool(exclusive)), _ptr(carry_in),
                              ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)), "scan_shard_scan")
+    return out
+
+
+def widen_copy(x: torch.Tensor, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """Measurement ceiling: out = widen(x), the scan's traffic with no scan arithmetic."""
+    dt, _, _ = _prep(x)
+    _check(load().scan_widen_copy(_ptr(x), _ptr(out), x.numel(), dt, _stream_ptr(stream)), "scan_widen_copy")
     return out
 
 

@@ -123,4 +123,55 @@ __global__ void k_carry_plus(const Sum* carry_in, const Sum* pre, int64_t idx, S
 }
 
 }  // namespace shard
+
+namespace ceiling {
+
+// The measurement ceiling of a scan: the same bytes (read In, write the widened
+// Out) with no arithmetic beyond the widening -- a grid-stride stream of
+// 16-byte loads and stores.  Not on any scan path; bench.py reports it next to
+// the scan so the roofline fraction can be read against what a pure stream of
+// the identical traffic achieves in the same run.
+template <int DT>
+__global__ void __launch_bounds__(256) k_widen_copy(const void* in_, void* out_, int64_t n)
+{
+    using Tr = Traits<DT>;
+    using In = typename Tr::In;
+    constexpr int VN = 16 / (int)sizeof(In);  // elements per 16-byte input vector
+    const In* in = reinterpret_cast<const In*>(in_);
+    uint32_t* out = reinterpret_cast<uint32_t*>(out_);
+    const int64_t nv = n / VN;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    auto emit = [&](int64_t i, const uint4& q) {
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+        uint32_t o[VN];
+#pragma unroll
+        for (int k = 0; k < VN; ++k) {
+            if constexpr (sizeof(In) == 4) o[k] = w[k];
+            else if constexpr (sizeof(In) == 2) o[k] = __float_as_uint(__half2float(__ushort_as_half((uint16_t)(w[k >> 1] >> (16 * (k & 1))))));
+            else o[k] = (uint32_t)(int32_t)(int8_t)(w[k >> 2] >> (8 * (k & 3)));
+        }
+#pragma unroll
+        for (int k = 0; k < VN; k += 4)
+            __stcs(reinterpret_cast<uint4*>(out + i * VN + k), make_uint4(o[k], o[k + 1], o[k + 2], o[k + 3]));
+    };
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; i + 3 * stride < nv; i += 4 * stride) {  // four 16-byte loads in flight per thread
+        const uint4 a = ptx::ld_stream_v4(reinterpret_cast<const uint4*>(in) + i);
+        const uint4 b = ptx::ld_stream_v4(reinterpret_cast<const uint4*>(in) + i + stride);
+        const uint4 c = ptx::ld_stream_v4(reinterpret_cast<const uint4*>(in) + i + 2 * stride);
+        const uint4 d = ptx::ld_stream_v4(reinterpret_cast<const uint4*>(in) + i + 3 * stride);
+        emit(i, a);
+        emit(i + stride, b);
+        emit(i + 2 * stride, c);
+        emit(i + 3 * stride, d);
+    }
+    for (; i < nv; i += stride) emit(i, ptx::ld_stream_v4(reinterpret_cast<const uint4*>(in) + i));
+    for (int64_t j = nv * VN + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += stride) {
+        if constexpr (sizeof(In) == 4) out[j] = reinterpret_cast<const uint32_t*>(in)[j];
+        else if constexpr (sizeof(In) == 2) out[j] = __float_as_uint(__half2float(__ushort_as_half(reinterpret_cast<const uint16_t*>(in)[j])));
+        else out[j] = (uint32_t)(int32_t)in[j];
+    }
+}
+
+}  // namespace ceiling
 }  // namespace scan

@@ -126,4 +126,24 @@ int scan_shard_scan(const void* in, void* out, int64_t n, int dtype, int exclusi
     return st;
 }
 
+int scan_widen_copy(const void* in, void* out, int64_t n, int dtype, void* stream)
+{
+    if (!valid_dt(dtype) || n < 0) return SCAN_ERR_ARG;
+    if (n == 0) return SCAN_OK;
+    if (in == nullptr || out == nullptr || ((uintptr_t)in & 15u) || ((uintptr_t)out & 15u)) return SCAN_ERR_ARG;
+    DevInfo di;
+    int st = dev_info(di);
+    if (st != SCAN_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned g = (unsigned)di.sms * 8;
+    switch (dtype) {
+    case SCAN_I32_I32: scan::ceiling::k_widen_copy<SCAN_I32_I32><<<g, 256, 0, s>>>(in, out, n); break;
+    case SCAN_F32_F32: scan::ceiling::k_widen_copy<SCAN_F32_F32><<<g, 256, 0, s>>>(in, out, n); break;
+    case SCAN_F16_F32: scan::ceiling::k_widen_copy<SCAN_F16_F32><<<g, 256, 0, s>>>(in, out, n); break;
+    default: scan::ceiling::k_widen_copy<SCAN_I8_I32><<<g, 256, 0, s>>>(in, out, n); break;
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+}
+
 }  // extern "C"
