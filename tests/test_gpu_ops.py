@@ -129,10 +129,11 @@ def test_radix_sort_parity(cuda, oracle, dt, desc):
         assert np.array_equal(out.cpu().numpy().view(bits), ro.view(bits)), (dt, n)
 
 
-def test_radix_sort_matches_torch_sort_stable(cuda):
+@pytest.mark.parametrize("n", [1 << 20, 1 << 24])  # 2^24 = bench_ops' sort workload
+def test_radix_sort_matches_torch_sort_stable(cuda, n):
     """Against torch.sort(stable=True) (CUB) on NaN-free keys without -0."""
     for dt in (torch.float16, torch.float32, torch.int32):
-        k = (torch.randn(1 << 20, device="cuda") * 1000).to(dt)
+        k = (torch.randn(n, device="cuda") * 1000).to(dt)
         if dt.is_floating_point:
             k[k == 0] = 1
         for desc in (False, True):
@@ -218,3 +219,24 @@ def test_top_p_select_edge_rows(cuda, oracle):
         for r in range(len(rows)):
             rt, rk = oracle.top_p_sample(P[r], p, float(u[r]))
             assert int(tok[r]) == rt and int(kept[r]) == rk, (p, r, int(tok[r]), rt, int(kept[r]), rk)
+
+
+@pytest.mark.slow
+def test_top_p_full_c4(cuda, oracle, inputs_mod):
+    """bench_ops' top-p workload (4096 C4 rows, p = 0.9): the sort-free path and
+    the sort path agree on every row; a sample of rows matches the oracle."""
+    R, C = 4096, 131072
+    P = torch.empty((R, C), dtype=torch.float32, device="cuda")
+    inputs_mod.fill_device(inputs_mod.F32_SOFTMAX, 3, 0, R, C, P)
+    u = torch.rand(R, generator=torch.Generator(device="cuda").manual_seed(7), device="cuda")
+    t1, k1 = cuda.top_p_sample(P, 0.9, u, method="select")
+    t2, k2 = cuda.top_p_sample(P, 0.9, u, method="sort")
+    # the sort path decides the nucleus on the fp32 row scan, the select path in
+    # fp64 (the oracle's precision): K may differ where C_j sits within fp32
+    # rounding of p; the drawn tokens agree
+    assert int((t1 != t2).sum()) <= 2 and int((k1 != k2).sum()) <= 16
+    uh = u.cpu().numpy()
+    for r in range(0, R, 256):
+        Ph = inputs_mod.fill_host(inputs_mod.F32_SOFTMAX, 3, r, 1, C)[0]
+        rt, rk = oracle.top_p_sample(Ph, 0.9, float(uh[r]))
+        assert int(t1[r]) == rt and int(k1[r]) == rk, (r, int(t1[r]), rt, int(k1[r]), rk)
