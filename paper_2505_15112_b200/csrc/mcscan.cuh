@@ -114,7 +114,7 @@ struct McParams16 {
     int64_t n_tma_out;      // elements covered by tm_out (full rows)
     int exclusive;
     int debug;
-    int ahead;              // reduce jobs run this many chunks ahead of scan jobs (1..2)
+    int ahead;              // reduce jobs run this many chunks ahead of scan jobs (1..4)
     int l2;                 // L2 policies: bits 0-1 Phase-I read, bits 2-3 Phase-II re-read (0 = default)
 };
 
@@ -454,8 +454,8 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     using Carry = typename Tr::Carry;
     constexpr int TILE = Cfg::kTile;
     constexpr int SZ = (int)sizeof(In);
-    constexpr int KC = 4;
-    constexpr int RS = 4;  // reduce-sum hand-off ring (ahead <= 2)
+    constexpr int KC = 8;  // carry ring (ahead <= 4)
+    constexpr int RS = 8;  // reduce-sum hand-off ring (ahead <= 4)
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* const smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);

@@ -260,7 +260,7 @@ struct Mc16Variant {
         p.ws = sp.ws;
         p.exclusive = sp.exclusive;
         p.debug = debug_bits();
-        p.ahead = ahead < 1 ? 1 : (ahead > 2 ? 2 : ahead);
+        p.ahead = ahead < 1 ? 1 : (ahead > 4 ? 4 : ahead);
         p.l2 = env_int("SCAN_MC_L2", 0);
         p.gm.n = n;
         p.gm.g = di.sms < kMaxGrid ? di.sms : kMaxGrid;
