@@ -6,6 +6,7 @@
 #include "sample.cuh"
 #include "topp.cuh"
 #include "split.cuh"
+#include "split_warp.cuh"
 #include "radix.cuh"
 
 namespace {
@@ -22,7 +23,16 @@ int64_t split_tiles(int64_t n) { return (n + kTile - 1) / kTile; }
 
 int64_t split_tiles4(int64_t n) { return (split_tiles(n) + 3) & ~(int64_t)3; }  // 16-byte aligned arrays
 
-size_t split_ws_bytes(int64_t n) { return kSplitArrays + (size_t)split_tiles4(n) * 8 + 64; }
+int64_t split_wtiles(int64_t n) { return (n + scan::splitw::kWT - 1) / scan::splitw::kWT; }
+
+size_t split_ws_bytes(int64_t n)
+{
+    // block kernel: counts + offs per 8192-tile; warp kernel: counts + loff per
+    // 4096-element warp tile + the CTA totals (<= 4096 CTAs)
+    const size_t a = (size_t)split_tiles4(n) * 8;
+    const size_t b = (size_t)((split_wtiles(n) + 3) & ~(int64_t)3) * 8 + 4096 * 4;
+    return kSplitArrays + (a > b ? a : b) + 64;
+}
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
@@ -90,9 +100,56 @@ int launch_split_tma(SplitParams& p, cudaStream_t s, const DevInfo& di)
     return launch_split_tma_c<SRC, ES, KT, IDX_IN, false>(p, s, di);
 }
 
+// Warp-granular split / compress (split_warp.cuh): int8 flags, 1- or 2-byte
+// payload, 16-byte aligned buffers.
+template <int ES>
+int launch_split_warp(const SplitParams& sp, cudaStream_t s, const DevInfo& di)
+{
+    using namespace scan::splitw;
+    WParams p;
+    memset(&p, 0, sizeof(p));
+    p.x = sp.x;
+    p.z = sp.z;
+    p.flags = sp.flags;
+    p.idx_out = sp.idx_out;
+    p.count_out = sp.count_out;
+    p.hdr = sp.hdr;
+    p.n = sp.n;
+    p.nwt = (int)split_wtiles(sp.n);
+    p.compress = sp.compress;
+    uint32_t* arr = sp.counts;  // the split workspace arrays region
+    const int64_t nwt4 = (p.nwt + 3) & ~3;
+    p.counts = arr;
+    p.loff = arr + nwt4;
+    p.cta_tot = arr + 2 * nwt4;
+    int grid = di.sms * 4;
+    if (grid > 4096) grid = 4096;
+    p.wpc = (p.nwt + grid - 1) / grid;
+    grid = (p.nwt + p.wpc - 1) / p.wpc;
+    k_splitw_count<<<(unsigned)grid, kThreads, 0, s>>>(p);
+    const int64_t want = ((int64_t)p.nwt + kWarps - 1) / kWarps;
+    const int64_t g2 = (int64_t)di.sms * 4 < want ? (int64_t)di.sms * 4 : want;
+    if (p.compress) {
+        if (p.idx_out) k_splitw_scatter<ES, true, true><<<(unsigned)g2, kThreads, 0, s>>>(p);
+        else k_splitw_scatter<ES, true, false><<<(unsigned)g2, kThreads, 0, s>>>(p);
+    } else {
+        if (p.idx_out) k_splitw_scatter<ES, false, true><<<(unsigned)g2, kThreads, 0, s>>>(p);
+        else k_splitw_scatter<ES, false, false><<<(unsigned)g2, kThreads, 0, s>>>(p);
+    }
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+}
+
 template <int SRC, int ES, int KT>
 int launch_split(SplitParams& p, cudaStream_t s, const DevInfo& di)
 {
+    if constexpr (SRC == scan::split::SRC_FLAGS && ES <= 2) {
+        // compress: the warp kernel (50 % vs 40 % of peak at 2^30); split with
+        // indices keeps the block kernel (67 % vs 53 %) -- measured, bench_ops.py
+        const char* e = getenv("SCAN_SPLIT_WARP");
+        const bool warp = e ? atoi(e) != 0 : p.compress != 0;
+        if (p.aligned && warp) return launch_split_warp<ES>(p, s, di);
+    }
     if constexpr (ES <= 4) {
         if (p.aligned && getenv("SCAN_SPLIT_NO_TMA") == nullptr) {
             if constexpr (SRC == scan::split::SRC_KEYBIT)

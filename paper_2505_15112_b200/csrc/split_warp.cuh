@@ -1,0 +1,257 @@
+// split_warp.cuh -- warp-granular split / compress (PAPER Sec. 5.1-5.2,
+// P281-285): the second-generation scatter for int8 flags and 1- or 2-byte
+// payloads (the paper's SplitInd case: "an array of 16-bit elements and a 0/1
+// mask array (flags are stored in int8)", P283).
+//
+// The block-level kernel (split.cuh) stages every tile in shared memory and
+// spends ~34 instructions per element on it.  Here a WARP owns a contiguous
+// "warp tile" of kWT elements and writes its outputs straight to global memory:
+//   * count pass: true count per warp tile; every CTA owns a contiguous range of
+//     warp tiles, scans its counts locally and publishes its total; the last
+//     CTA scans the CTA totals (a two-level exclusive scan, no serial pass over
+//     all tiles);
+//   * scatter pass: per step a warp reads 128 consecutive elements (4 per lane:
+//     one 4-byte flag word, one 8-/4-byte payload word), the in-step exclusive
+//     scan of the mask is 4 ballots + popcounts (lanes own consecutive
+//     elements, so the order of the run is lane-major); the step is staged in
+//     output order in a 128-word per-warp buffer and written back by
+//     consecutive lanes: trues to off + (trues before), falses to
+//     T + (warp tile start - off) + (falses before) -- P283's offsets -- as
+//     coalesced runs, no block-level barrier.
+// HBM bytes per element as before (mask twice, payload once in and out,
+// indices out); instructions per element ~8 instead of ~34.
+#pragma once
+#include <stdint.h>
+
+#include "ptx.cuh"
+
+namespace scan {
+namespace splitw {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kWT = 4096;             // elements per warp tile
+constexpr int kStep = 128;            // elements per warp step (4 per lane)
+constexpr int kSteps = kWT / kStep;   // 32
+constexpr int kAhead = 4;             // steps in flight per warp
+
+struct WParams {
+    const void* x;          // payload
+    void* z;                // output
+    const int8_t* flags;
+    int32_t* idx_out;       // nullable
+    int64_t* count_out;     // nullable, device: T
+    uint32_t* counts;       // [nwt] true count per warp tile
+    uint32_t* loff;         // [nwt] exclusive scan of counts within the owning CTA's range
+    uint32_t* cta_tot;      // [grid] CTA totals, then (last CTA) their exclusive scan
+    uint32_t* hdr;          // [0] done counter, [2..3] T
+    int64_t n;
+    int nwt;                // warp tiles
+    int wpc;                // warp tiles per count CTA (contiguous)
+    int compress;
+};
+
+__device__ __forceinline__ uint32_t nz_bits4(uint32_t f)
+{
+    // bit j = byte j of f is nonzero (R12)
+    const uint32_t nz = __vcmpne4(f, 0u) & 0x80808080u;
+    return (nz * 0x00204081u) >> 28;
+}
+
+// ---- count pass ------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_splitw_count(const WParams p)
+{
+    __shared__ uint32_t s_red[kWarps];
+    __shared__ bool s_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wt0 = blockIdx.x * p.wpc;
+    const int wt1 = min(p.nwt, wt0 + p.wpc);
+    for (int wt = wt0 + warp; wt < wt1; wt += kWarps) {
+        const int64_t e0 = (int64_t)wt * kWT;
+        uint32_t c = 0;
+        if (e0 + kWT <= p.n) {
+            const uint4* v = reinterpret_cast<const uint4*>(p.flags + e0);
+            uint4 q[kWT / 512];
+#pragma unroll
+            for (int k = 0; k < kWT / 512; ++k) q[k] = ptx::ld_stream_v4(v + k * 32 + lane);
+#pragma unroll
+            for (int k = 0; k < kWT / 512; ++k)
+                c += __popc(__vcmpne4(q[k].x, 0u) & 0x01010101u) + __popc(__vcmpne4(q[k].y, 0u) & 0x01010101u) +
+                     __popc(__vcmpne4(q[k].z, 0u) & 0x01010101u) + __popc(__vcmpne4(q[k].w, 0u) & 0x01010101u);
+        } else {
+            for (int64_t e = e0 + lane; e < p.n; e += 32) c += p.flags[e] != 0 ? 1u : 0u;
+        }
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (lane == 0) p.counts[wt] = c;
+    }
+    __syncthreads();
+    // CTA-local exclusive scan of this CTA's contiguous range of counts
+    uint32_t carry = 0;
+    for (int base = wt0; base < wt1; base += kThreads) {
+        const int i = base + tid;
+        const uint32_t x = i < wt1 ? p.counts[i] : 0u;
+        uint32_t incl = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += y;
+        }
+        if (lane == 31) s_red[warp] = incl;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t y = s_red[w];
+            if (w < warp) wpre += y;
+            tot += y;
+        }
+        if (i < wt1) p.loff[i] = carry + wpre + incl - x;
+        carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) p.cta_tot[blockIdx.x] = carry;
+    // last CTA: exclusive scan of the CTA totals
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&p.hdr[0], 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    uint64_t run = 0;
+    for (int base = 0; base < (int)gridDim.x; base += kThreads) {
+        const int i = base + tid;
+        const uint32_t x = i < (int)gridDim.x ? __ldcg(&p.cta_tot[i]) : 0u;
+        uint32_t incl = x;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+            if (lane >= d) incl += y;
+        }
+        if (lane == 31) s_red[warp] = incl;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t y = s_red[w];
+            if (w < warp) wpre += y;
+            tot += y;
+        }
+        __syncthreads();
+        if (i < (int)gridDim.x) p.cta_tot[i] = (uint32_t)(run + wpre + incl - x);
+        run += tot;
+    }
+    if (tid == 0) {
+        reinterpret_cast<uint64_t*>(p.hdr)[1] = run;
+        if (p.count_out) *p.count_out = (int64_t)run;
+        p.hdr[0] = 0;
+    }
+}
+
+// ---- scatter pass: a warp per warp tile, direct predicated stores -------------
+template <int ES, bool CMP, bool IDX>
+__global__ void __launch_bounds__(kThreads) k_splitw_scatter(const WParams p)
+{
+    using P = typename std::conditional<ES == 2, uint16_t, uint8_t>::type;
+    using PV = typename std::conditional<ES == 2, uint2, uint32_t>::type;  // 4 payload elements
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * kThreads) >> 5;
+    const uint64_t T = reinterpret_cast<const uint64_t*>(p.hdr)[1];
+    const uint32_t lt = (1u << lane) - 1u;
+    P* const z = reinterpret_cast<P*>(p.z);
+    __shared__ uint32_t s_wbuf[kWarps][kStep];
+    uint32_t* const wbuf = s_wbuf[threadIdx.x >> 5];
+    for (int wt = gw; wt < p.nwt; wt += nw) {
+        const int64_t e0 = (int64_t)wt * kWT;
+        const uint64_t off = (uint64_t)__ldg(&p.cta_tot[wt / p.wpc]) + __ldg(&p.loff[wt]);
+        uint64_t tpos = off;                             // next true slot
+        uint64_t fpos = T + (uint64_t)e0 - off;          // next false slot
+        const bool full = e0 + kWT <= p.n;
+        if (full) {
+            const uint32_t* fw = reinterpret_cast<const uint32_t*>(p.flags + e0);
+            const PV* pw = reinterpret_cast<const PV*>(reinterpret_cast<const P*>(p.x) + e0);
+            uint32_t fq[kAhead];
+            PV pq[kAhead];
+#pragma unroll
+            for (int a = 0; a < kAhead; ++a) {
+                fq[a] = __ldcs(fw + a * 32 + lane);
+                pq[a] = __ldcs(pw + a * 32 + lane);
+            }
+#pragma unroll 1
+            for (int st = 0; st < kSteps; st += kAhead) {
+#pragma unroll
+                for (int a = 0; a < kAhead; ++a) {
+                    const uint32_t f = fq[a];
+                    const PV pv = pq[a];
+                    const int nx = st + a + kAhead;  // prefetch the step kAhead ahead
+                    if (nx < kSteps) {
+                        fq[a] = __ldcs(fw + nx * 32 + lane);
+                        pq[a] = __ldcs(pw + nx * 32 + lane);
+                    }
+                    const uint32_t bits = nz_bits4(f);
+                    const uint32_t b0 = __ballot_sync(0xffffffffu, bits & 1u);
+                    const uint32_t b1 = __ballot_sync(0xffffffffu, bits & 2u);
+                    const uint32_t b2 = __ballot_sync(0xffffffffu, bits & 4u);
+                    const uint32_t b3 = __ballot_sync(0xffffffffu, bits & 8u);
+                    const uint32_t before = __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+                    const uint32_t tot = __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+                    uint32_t pw32[2];
+                    if constexpr (ES == 2) { pw32[0] = pv.x; pw32[1] = pv.y; }
+                    else { pw32[0] = pv; pw32[1] = 0; }
+                    // stage the step in output order (trues, then falses) in this
+                    // warp's 128-word buffer: (payload << 16) | element-in-step
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint32_t val;
+                        if constexpr (ES == 2) val = (pw32[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+                        else val = (pw32[0] >> (8 * j)) & 0xffu;
+                        const uint32_t tb = before + __popc(bits & ((1u << j) - 1u));  // trues before element j
+                        const uint32_t slot = ((bits >> j) & 1u) ? tb : tot + (uint32_t)(4 * lane + j) - tb;
+                        if (!CMP || ((bits >> j) & 1u)) wbuf[slot] = (val << 16) | (uint32_t)(4 * lane + j);
+                    }
+                    __syncwarp();
+                    // write consecutive slots from consecutive lanes: coalesced runs
+                    const int64_t sbase = e0 + (int64_t)(st + a) * kStep;
+                    const int lim = CMP ? (int)tot : kStep;
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) {
+                        const int k = r * 32 + lane;
+                        if (k < lim) {
+                            const uint32_t w = wbuf[k];
+                            const uint64_t d = k < (int)tot ? tpos + k : fpos + (uint64_t)(k - (int)tot);
+                            z[d] = (P)(w >> 16);
+                            if constexpr (IDX) p.idx_out[d] = (int32_t)(sbase + (w & 0xffffu));
+                        }
+                    }
+                    __syncwarp();
+                    tpos += tot;
+                    fpos += kStep - tot;
+                }
+            }
+        } else {
+            // ragged last warp tile: element by element, same order
+            for (int64_t s0 = e0; s0 < p.n; s0 += 32) {
+                const int64_t e = s0 + lane;
+                const bool ok = e < p.n;
+                const bool tr = ok && p.flags[e] != 0;
+                const P val = ok ? reinterpret_cast<const P*>(p.x)[e] : (P)0;
+                const uint32_t bt = __ballot_sync(0xffffffffu, tr);
+                const uint32_t bv = __ballot_sync(0xffffffffu, ok);
+                if (tr) {
+                    const uint64_t d = tpos + __popc(bt & lt);
+                    z[d] = val;
+                    if constexpr (IDX) p.idx_out[d] = (int32_t)e;
+                } else if (ok && !CMP) {
+                    const uint64_t d = fpos + __popc(bv & ~bt & lt);
+                    z[d] = val;
+                    if constexpr (IDX) p.idx_out[d] = (int32_t)e;
+                }
+                tpos += __popc(bt);
+                fpos += __popc(bv & ~bt);
+            }
+        }
+    }
+}
+
+}  // namespace splitw
+}  // namespace scan

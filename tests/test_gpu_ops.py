@@ -28,7 +28,10 @@ def _payload(n, es, seed):
 
 @pytest.mark.parametrize("es", [1, 2, 4, 8])
 @pytest.mark.parametrize("compress", [False, True])
-def test_split_sizes(cuda, oracle, inputs_mod, es, compress):
+@pytest.mark.parametrize("kernel", ["default", "warp", "block"])
+def test_split_sizes(cuda, oracle, inputs_mod, monkeypatch, es, compress, kernel):
+    if kernel != "default":  # both scatter kernels, whichever the default picks
+        monkeypatch.setenv("SCAN_SPLIT_WARP", "1" if kernel == "warp" else "0")
     for n in SIZES:
         f = _flags(inputs_mod, n, seed=n)
         xd, xh = _payload(n, es, seed=n + es)
