@@ -453,8 +453,14 @@ int launch_dt(ScanParams p, cudaStream_t s, const DevInfo& di)
     const int v = variant();
     if (v == 0 || p.seg_len <= Small::kTile) {
         if (p.seg_len <= Small::kTile) return Small::launch(p, s, di);
-        if (p.num_segs == 1 && p.seg_len <= 16 * (int64_t)Small::kTile && env_int("SCAN_NO_CLUSTER", 0) == 0)
+        if (p.num_segs == 1 && p.seg_len <= 16 * (int64_t)Small::kTile && env_int("SCAN_NO_CLUSTER", 0) == 0) {
+            // n <= 65,536 (C1): 4096-element tiles, up to 16 CTAs in the cluster --
+            // half the per-CTA latency of 8192-element tiles (C1 step 12.1 -> 9-10 us)
+            using Small4 = Variant<DT, 256, 4, 2, 1, 2>;
+            if (env_int("SCAN_SMALL4", 1) != 0 && p.seg_len <= 16 * (int64_t)Small4::kTile)
+                return Small4::launch_cluster(p, s);
             return Small::launch_cluster(p, s);
+        }
         if (p.num_segs == 1 && p.tma_in && p.tma_out && p.seg_len >= kMcMinElems &&
             env_int("SCAN_NO_MC", 0) == 0)
             return launch_mc<DT>(p, s, di);
