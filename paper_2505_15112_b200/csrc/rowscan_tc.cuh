@@ -35,14 +35,24 @@ namespace tc {
 constexpr int kCols = 16384;       // elements per row = one 128 x 128 tile
 constexpr int kNA = 2;             // input tile ring
 constexpr int kThreads = 10 * 32;  // TMA, MMA, two epilogue groups of 4 warps
-constexpr uint32_t kTileBytes = kCols * 2;    // 32 KB of fp16
-constexpr uint32_t kHalfBytes = kTileBytes / 2;  // one 64-wide K block: [128 rows x 128 B]
-constexpr uint32_t kOutBytes = kCols * 4;       // 64 KB fp32 output tile (staging)
-constexpr size_t kSmem = kTileBytes /*T*/ + kNA * kTileBytes + 2 * kOutBytes;  // 2 groups x 2 half-tile buffers
+constexpr uint32_t kKBlock = 128 * 128;         // one 128-byte-wide K block: [128 rows x 128 B]
+constexpr uint32_t kOutBytes = kCols * 4;       // 64 KB fp32 / int32 output tile (staging)
+// ES = 2: fp16 in (kind::f16, 2 K blocks of 64, 8 MMAs of K = 16);
+// ES = 1: int8 in (kind::i8, 1 K block of 128, 4 MMAs of K = 32), exact int32 sums.
+template <int ES>
+struct TcCfg {
+    static constexpr uint32_t kTileBytes = kCols * ES;
+    static constexpr int kKBlocks = ES;                 // 128-byte K blocks per tile row
+    static constexpr int kKPerMma = 16 * (3 - ES);      // 16 (f16) / 32 (i8) elements
+    static constexpr int kMmaPerBlock = 128 / ES / kKPerMma;  // 4 per K block
+    static constexpr size_t kSmem = kTileBytes /*T*/ + kNA * kTileBytes + 2 * kOutBytes;
+};
+constexpr uint32_t kTileBytes = kCols * 2;    // fp16 (kept for the host launcher)
+constexpr size_t kSmem = TcCfg<2>::kSmem;
 
 struct TcParams {
     CUtensorMap tm_in;   // 3-D {128 fp16, 128 chunks, rows}, box {64, 128, 1}, SWIZZLE_128B
-    float* out;
+    void* out;           // fp32 (fp16 input) or int32 (int8 input)
     int64_t rows;
     int64_t out_stride;  // elements
 };
@@ -60,8 +70,11 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t smem_addr)
     return d;
 }
 
-// kind::f16 instruction descriptor: D fp32, A/B fp16, both K-major, N = M = 128.
+// Instruction descriptors, both operands K-major, N = M = 128:
+// kind::f16: D fp32 (c_format 1), A/B fp16 (format 0);
+// kind::i8:  D s32 (c_format 2), A/B signed int8 (format 1).
 constexpr uint32_t kIdesc = (1u << 4) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t kIdescI8 = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 
 __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate)
 {
@@ -71,6 +84,14 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b,
         "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
 }
 
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(kIdescI8), "r"(accumulate));
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t* bar)
 {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -78,7 +99,7 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar)
                  : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32])
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32])
 {
     uint32_t r[32];
     asm volatile(
@@ -90,7 +111,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32])
           "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 #pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+    for (int i = 0; i < 32; ++i) v[i] = r[i];
 }
 
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
@@ -107,18 +128,27 @@ __device__ __forceinline__ void tma_load_3d_tc(void* dst, const CUtensorMap* tm,
         : "memory");
 }
 
+template <typename V>
+struct alignas(16) V4 {
+    V x, y, z, w;
+};
+
+template <int ES>
 __global__ void __launch_bounds__(kThreads, 1) k_rowscan_tc(const __grid_constant__ TcParams p)
 {
+    using C = TcCfg<ES>;
+    using V = typename std::conditional<ES == 2, float, uint32_t>::type;  // accumulator / output type
+    constexpr uint32_t kTB = C::kTileBytes;
     extern __shared__ __align__(1024) uint8_t smem_raw[];  // SWIZZLE_128B operands need 1024-B alignment
     uint8_t* const base = smem_raw;
-    uint8_t* const sT = base;                  // T = U^T operand, 2 K-blocks of 16 KB
-    uint8_t* const sX = base + kTileBytes;     // kNA input tiles
-    float* const sO0 = reinterpret_cast<float*>(base + kTileBytes + kNA * kTileBytes);  // output staging x2
+    uint8_t* const sT = base;                  // T = U^T operand, ES K-blocks of 16 KB
+    uint8_t* const sX = base + kTB;            // kNA input tiles
+    V* const sO0 = reinterpret_cast<V*>(base + kTB + kNA * kTB);  // output staging x2
 
     __shared__ __align__(8) uint64_t a_full[kNA], a_empty[kNA], t_full[2], t_empty[2];
     __shared__ uint32_t s_tmem;
-    __shared__ __align__(16) float s_tot[2][128];   // per epilogue group
-    __shared__ __align__(16) float s_base[2][128];
+    __shared__ __align__(16) V s_tot[2][128];   // per epilogue group
+    __shared__ __align__(16) V s_base[2][128];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -126,9 +156,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_rowscan_tc(const __grid_constan
     // j*128 B, 16-byte chunk c = (k%64)/8 stored at chunk c ^ (j % 8).
     for (int e = tid; e < 128 * 128; e += kThreads) {
         const int j = e >> 7, k = e & 127;
-        const int kb = k >> 6, kk = k & 63;
-        const uint32_t off = kb * kHalfBytes + j * 128 + ((((kk >> 3) ^ (j & 7)) << 4)) + (kk & 7) * 2;
-        *reinterpret_cast<uint16_t*>(sT + off) = (k <= j) ? (uint16_t)0x3C00 : (uint16_t)0;
+        if constexpr (ES == 2) {  // fp16 1.0, K blocks of 64 elements
+            const int kb = k >> 6, kk = k & 63;
+            const uint32_t off = kb * kKBlock + j * 128 + ((((kk >> 3) ^ (j & 7)) << 4)) + (kk & 7) * 2;
+            *reinterpret_cast<uint16_t*>(sT + off) = (k <= j) ? (uint16_t)0x3C00 : (uint16_t)0;
+        } else {                  // int8 1, one K block of 128 elements
+            const uint32_t off = j * 128 + ((((k >> 4) ^ (j & 7)) << 4)) + (k & 15);
+            sT[off] = (k <= j) ? (uint8_t)1 : (uint8_t)0;
+        }
     }
     if (tid == 0) {
         for (int s = 0; s < kNA; ++s) {
@@ -161,10 +196,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_rowscan_tc(const __grid_constan
             bool wrapped = false;
             for (int64_t r = blockIdx.x; r < p.rows; r += gridDim.x) {
                 if (wrapped) ptx::mbar_wait(&a_empty[s], ph ^ 1u);
-                uint8_t* dst = sX + s * kTileBytes;
-                ptx::mbar_arrive_expect_tx(&a_full[s], kTileBytes);
-                tma_load_3d_tc(dst, &p.tm_in, 0, 0, (int)r, &a_full[s], pol);
-                tma_load_3d_tc(dst + kHalfBytes, &p.tm_in, 64, 0, (int)r, &a_full[s], pol);
+                uint8_t* dst = sX + s * kTB;
+                ptx::mbar_arrive_expect_tx(&a_full[s], kTB);
+#pragma unroll
+                for (int kb = 0; kb < C::kKBlocks; ++kb)
+                    tma_load_3d_tc(dst + kb * kKBlock, &p.tm_in, kb * (128 / ES), 0, (int)r, &a_full[s], pol);
                 if (++s == kNA) {
                     s = 0;
                     ph ^= 1u;
@@ -184,15 +220,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_rowscan_tc(const __grid_constan
                 if (i >= 2) ptx::mbar_wait(&t_empty[b], (uint32_t)((i >> 1) - 1) & 1u);
                 ptx::mbar_wait(&a_full[s], ph);
                 tc_fence_after();
-                const uint32_t x_addr = ptx::smem_u32(sX + s * kTileBytes);
+                const uint32_t x_addr = ptx::smem_u32(sX + s * kTB);
                 const uint32_t d = tmem + (uint32_t)(b * 128);
 #pragma unroll
-                for (int kb = 0; kb < 2; ++kb) {
+                for (int kb = 0; kb < C::kKBlocks; ++kb) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint64_t a = sw128_desc(t_addr + kb * kHalfBytes + k * 32);
-                        const uint64_t bb = sw128_desc(x_addr + kb * kHalfBytes + k * 32);
-                        mma_f16(d, a, bb, (kb | k) != 0);
+                    for (int k = 0; k < C::kMmaPerBlock; ++k) {  // 32 bytes of K per MMA
+                        const uint64_t a = sw128_desc(t_addr + kb * kKBlock + k * 32);
+                        const uint64_t bb = sw128_desc(x_addr + kb * kKBlock + k * 32);
+                        if constexpr (ES == 2) mma_f16(d, a, bb, (kb | k) != 0);
+                        else mma_i8(d, a, bb, (kb | k) != 0);
                     }
                 }
                 mma_commit(&a_empty[s]);  // input slot free once these MMAs have read it
@@ -212,21 +249,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_rowscan_tc(const __grid_constan
         const int g = (warp - 2) >> 2;         // epilogue group
         const int ew = (warp - 2) & 3;         // warp within the group
         const int bar_id = 1 + g;
-        float* const sO = sO0 + g * (kOutBytes / 4);  // this group's two 32 KB half-tile buffers
+        V* const sO = sO0 + g * (kOutBytes / 4);  // this group's two 32 KB half-tile buffers
         int hb = 0;                                    // next half buffer
         int64_t i = g;
         for (int64_t r = blockIdx.x + (int64_t)g * gridDim.x; r < p.rows; r += 2 * (int64_t)gridDim.x, i += 2) {
             const int b = g;
             ptx::mbar_wait(&t_full[b], (uint32_t)(i >> 1) & 1u);
             tc_fence_after();
-            float v[128];
+            V v[128];
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * 128);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-                float w[32];
+                uint32_t w[32];
                 tmem_ld32(ta + c * 32, w);
 #pragma unroll
-                for (int t = 0; t < 32; ++t) v[c * 32 + t] = w[t];
+                for (int t = 0; t < 32; ++t) {
+                    if constexpr (ES == 2) v[c * 32 + t] = __uint_as_float(w[t]);
+                    else v[c * 32 + t] = w[t];
+                }
             }
             tmem_wait_ld();
             tc_fence_before();
@@ -235,20 +275,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_rowscan_tc(const __grid_constan
             if (j == 127) {
 #pragma unroll
                 for (int m = 0; m < 128; m += 4)
-                    *reinterpret_cast<float4*>(&s_tot[b][m]) = make_float4(v[m], v[m + 1], v[m + 2], v[m + 3]);
+                    *reinterpret_cast<V4<V>*>(&s_tot[b][m]) = V4<V>{v[m], v[m + 1], v[m + 2], v[m + 3]};
             }
             ptx::named_bar_sync(bar_id, 128);
             if (ew == 0) {
-                const float4 t4 = *reinterpret_cast<const float4*>(&s_tot[b][lane * 4]);
-                const float l0 = t4.x, l1 = l0 + t4.y, l2 = l1 + t4.z, l3 = l2 + t4.w;
-                float incl = l3;
+                const V4<V> t4 = *reinterpret_cast<const V4<V>*>(&s_tot[b][lane * 4]);
+                const V l0 = t4.x, l1 = l0 + t4.y, l2 = l1 + t4.z, l3 = l2 + t4.w;
+                V incl = l3;
 #pragma unroll
                 for (int d = 1; d < 32; d <<= 1) {
-                    const float y = __shfl_up_sync(0xffffffffu, incl, d);
+                    const V y = __shfl_up_sync(0xffffffffu, incl, d);
                     if (lane >= d) incl += y;
                 }
-                const float ex = incl - l3;
-                *reinterpret_cast<float4*>(&s_base[b][lane * 4]) = make_float4(ex, ex + l0, ex + l1, ex + l2);
+                V ex = __shfl_up_sync(0xffffffffu, incl, 1);
+                if (lane == 0) ex = V(0);
+                *reinterpret_cast<V4<V>*>(&s_base[b][lane * 4]) = V4<V>{ex, ex + l0, ex + l1, ex + l2};
                 if (lane == 0) ptx::bulk_wait_read<1>();  // buffer hb's previous store has read it
             }
             ptx::named_bar_sync(bar_id, 128);
@@ -260,10 +301,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_rowscan_tc(const __grid_constan
                     if (ew == 0 && lane == 0) ptx::bulk_wait_read<1>();
                     ptx::named_bar_sync(bar_id, 128);
                 }
-                float* const buf = sO + hb * (kOutBytes / 8);
+                V* const buf = sO + hb * (kOutBytes / 8);
 #pragma unroll
                 for (int m = 64 * h; m < 64 * h + 64; m += 4) {
-                    const float4 bs = *reinterpret_cast<const float4*>(&s_base[b][m]);
+                    const V4<V> bs = *reinterpret_cast<const V4<V>*>(&s_base[b][m]);
                     const int mm = m - 64 * h;
                     buf[(mm + 0) * 128 + j] = bs.x + v[m + 0];
                     buf[(mm + 1) * 128 + j] = bs.y + v[m + 1];
@@ -273,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rowscan_tc(const __grid_constan
                 ptx::fence_proxy_async_smem();
                 ptx::named_bar_sync(bar_id, 128);
                 if (ew == 0 && lane == 0) {
-                    ptx::tma_store_1d(p.out + r * p.out_stride + h * 64 * 128, buf, kOutBytes / 2,
+                    ptx::tma_store_1d(reinterpret_cast<V*>(p.out) + r * p.out_stride + h * 64 * 128, buf, kOutBytes / 2,
                                       ptx::policy_evict_first());
                     ptx::bulk_commit();
                 }

@@ -398,32 +398,35 @@ bool rowscan_ok(const ScanParams& p)
 
 // Tensor-core local scan (rowscan_tc.cuh), the A/B of SURVEY 8(f) row 2:
 // fp16 rows of exactly 16,384 elements, inclusive, selected by SCAN_ROWS_TC=1.
+template <int ES>
 int launch_rows_tc(const ScanParams& sp, cudaStream_t s, const DevInfo& di)
 {
+    using Cfg = scan::tc::TcCfg<ES>;
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     std::call_once(once, [] {
-        err = cudaFuncSetAttribute(scan::tc::k_rowscan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)scan::tc::kSmem);
+        err = cudaFuncSetAttribute(scan::tc::k_rowscan_tc<ES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)Cfg::kSmem);
     });
     if (err != cudaSuccess) return SCAN_ERR_CUDA;
     EncodeTiledFn fn = encode_fn();
     if (!fn) return SCAN_ERR_CUDA;
     scan::tc::TcParams p;
     memset(&p, 0, sizeof(p));
+    // [rows][128 chunks][128 elements] view, boxes of one 128-byte K block x 128 chunks
     const cuuint64_t dims[3] = {128, 128, (cuuint64_t)sp.num_segs};
-    const cuuint64_t strides[2] = {256, (cuuint64_t)(sp.in_stride * 2)};
-    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint64_t strides[2] = {128 * ES, (cuuint64_t)(sp.in_stride * ES)};
+    const cuuint32_t box[3] = {128 / ES, 128, 1};
     const cuuint32_t es[3] = {1, 1, 1};
-    if (fn(&p.tm_in, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(sp.in), dims, strides, box, es,
-           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    if (fn(&p.tm_in, ES == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_UINT8, 3,
+           const_cast<void*>(sp.in), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return SCAN_ERR_CUDA;
-    p.out = reinterpret_cast<float*>(sp.out);
+    p.out = sp.out;
     p.rows = sp.num_segs;
     p.out_stride = sp.out_stride;
     const int64_t grid = di.sms < sp.num_segs ? di.sms : sp.num_segs;
-    scan::tc::k_rowscan_tc<<<(unsigned)grid, scan::tc::kThreads, scan::tc::kSmem, s>>>(p);
+    scan::tc::k_rowscan_tc<ES><<<(unsigned)grid, scan::tc::kThreads, Cfg::kSmem, s>>>(p);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
 }
@@ -431,9 +434,9 @@ int launch_rows_tc(const ScanParams& sp, cudaStream_t s, const DevInfo& di)
 template <int DT>
 int launch_rows(const ScanParams& p, cudaStream_t s, const DevInfo& di)
 {
-    if constexpr (DT == SCAN_F16_F32) {
-        if (p.seg_len == scan::tc::kCols && !p.exclusive && env_int("SCAN_ROWS_TC", 0) != 0)
-            return launch_rows_tc(p, s, di);
+    if constexpr (DT == SCAN_F16_F32 || DT == SCAN_I8_I32) {  // tensor-core A/B (SCAN_ROWS_TC=1)
+        if (p.seg_len == scan::tc::kCols && !p.exclusive && p.row_pre == nullptr && env_int("SCAN_ROWS_TC", 0) != 0)
+            return launch_rows_tc<DT == SCAN_F16_F32 ? 2 : 1>(p, s, di);
     }
     switch (env_int("SCAN_ROWS", 0)) {
     case 1: return RowVariant<DT, 16, 1, 6>::launch(p, s, di);

@@ -31,3 +31,15 @@ def test_rowscan_tc_strided(cuda, oracle, inputs_mod, monkeypatch):
     for r in range(7):
         y64, a64, _ = oracle.inclusive(np.ascontiguousarray(h[r, :C]), "f16")
         assert oracle.check_f32(got[r], y64, a64)[0] == 0
+
+
+@pytest.mark.parametrize("rows", [1, 5, 148, 300])
+def test_rowscan_tc_int8_bit_exact(cuda, oracle, inputs_mod, monkeypatch, rows):
+    """kind::i8 (exact int32 accumulation): bit-exact for flags and full-range int8."""
+    monkeypatch.setenv("SCAN_ROWS_TC", "1")
+    C = 16384
+    for kind, seed in ((inputs_mod.I8_FLAG, 2), (inputs_mod.I8_FULL, 6)):
+        h = inputs_mod.fill_host(kind, seed, 0, rows * C).reshape(rows, C)
+        got = cuda.rows(torch.from_numpy(h).cuda()).cpu().numpy()
+        ref = oracle.rows(h, "i8")
+        assert np.array_equal(got, ref), rows
