@@ -16,6 +16,7 @@
 #include "mcscan.cuh"
 #include "rowscan.cuh"
 #include "rowscan_tc.cuh"
+#include "rows_small.cuh"
 
 using namespace scan;
 
@@ -449,11 +450,54 @@ int launch_rows(const ScanParams& p, cudaStream_t s, const DevInfo& di)
 // path for multi-tile segments is the warp-specialized kernel.  SCAN_VARIANT
 // selects alternatives for experiments.
 template <int DT>
+int launch_rows_small(const ScanParams& sp, cudaStream_t s, const DevInfo& di)
+{
+    using namespace scan::rows_small;
+    SRParams p;
+    p.in = sp.in;
+    p.out = sp.out;
+    p.rows = sp.num_segs;
+    p.cols = sp.seg_len;
+    p.in_stride = sp.in_stride;
+    p.out_stride = sp.out_stride;
+    p.exclusive = sp.exclusive;
+    const bool contig = sp.in_stride == sp.seg_len && sp.out_stride == sp.seg_len &&
+                        ((reinterpret_cast<uintptr_t>(sp.in) | reinterpret_cast<uintptr_t>(sp.out)) & 15) == 0;
+    if (sp.seg_len <= kTileMaxCols && contig && env_int("SCAN_ROWS_TILE", 1)) {
+        int64_t grid = (sp.num_segs + kThreads - 1) / kThreads;
+        const int64_t cap = (int64_t)di.sms * 6;  // 34 KB of shared memory per CTA
+        if (grid > cap) grid = cap;
+        k_rows_tile<DT><<<(unsigned)grid, kThreads, 0, s>>>(p);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+    }
+    int64_t warps_needed;
+    if (sp.seg_len <= 32) {
+        int G = 1;
+        while (G < sp.seg_len) G <<= 1;
+        warps_needed = (sp.num_segs + (32 / G) - 1) / (32 / G);
+    } else {
+        warps_needed = sp.num_segs;
+    }
+    int64_t grid = (warps_needed + kWarps - 1) / kWarps;
+    const int64_t cap = (int64_t)di.sms * 8;  // 8 CTAs of 8 warps per SM
+    if (grid > cap) grid = cap;
+    if (sp.seg_len <= 32) k_rows_tiny<DT><<<(unsigned)grid, kThreads, 0, s>>>(p);
+    else k_rows_warp<DT><<<(unsigned)grid, kThreads, 0, s>>>(p);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+}
+
+template <int DT>
 int launch_dt(ScanParams p, cudaStream_t s, const DevInfo& di)
 {
     constexpr bool wide_in = (DT == SCAN_I32_I32 || DT == SCAN_F32_F32);
     using Small = Variant<DT, 512, 4, 2, 1, 2>;  // 8192-element tiles
     const int v = variant();
+    // batched short rows: a warp (or a fraction of one) per row -- SURVEY 8(a) a6
+    if (p.num_segs > 1 && p.seg_len <= env_int("SCAN_ROWS_WARP_MAX", 4096) && p.carry_in == nullptr &&
+        p.row_pre == nullptr && v == 0)
+        return launch_rows_small<DT>(p, s, di);
     if (v == 0 || p.seg_len <= Small::kTile) {
         if (p.seg_len <= Small::kTile) return Small::launch(p, s, di);
         if (p.num_segs == 1 && p.seg_len <= 16 * (int64_t)Small::kTile && env_int("SCAN_NO_CLUSTER", 0) == 0) {
@@ -467,7 +511,25 @@ int launch_dt(ScanParams p, cudaStream_t s, const DevInfo& di)
         if (p.num_segs == 1 && p.tma_in && p.tma_out && p.seg_len >= kMcMinElems &&
             env_int("SCAN_NO_MC", 0) == 0)
             return launch_mc<DT>(p, s, di);
-        if (rowscan_ok<DT>(p)) return launch_rows<DT>(p, s, di);
+        // few long rows (fewer than half the SMs, >= 2^22 elements each): one
+        // full-GPU MCScan per row instead of one CTA per row -- SURVEY 8(a) a6
+        const int few = env_int("SCAN_FEW_ROWS", 0);
+        if (p.num_segs > 1 && p.num_segs * 2 <= di.sms && p.seg_len >= ((int64_t)1 << 22) && p.tma_in &&
+            p.tma_out && p.row_pre == nullptr && env_int("SCAN_NO_MC", 0) == 0 && few == 0) {
+            using In = typename Traits<DT>::In;
+            for (int64_t r = 0; r < p.num_segs; ++r) {
+                ScanParams q = p;
+                q.in = (const uint8_t*)p.in + r * p.in_stride * (int64_t)sizeof(In);
+                q.out = (uint8_t*)p.out + r * p.out_stride * 4;
+                q.num_segs = 1;
+                q.in_stride = q.out_stride = p.seg_len;
+                q.carry_in = nullptr;
+                const int st = launch_mc<DT>(q, s, di);
+                if (st != SCAN_OK) return st;
+            }
+            return SCAN_OK;
+        }
+        if (rowscan_ok<DT>(p) && !(few == 1 && p.num_segs < di.sms)) return launch_rows<DT>(p, s, di);
         if constexpr (wide_in) {
             return WsVariant<DT, 16, 3, 8, 3, 3>::launch(p, s, di);
         } else if constexpr (DT == SCAN_F16_F32) {

@@ -346,3 +346,27 @@ def test_shard_two_pass(cuda, oracle, inputs_mod, dt, exclusive):
             c = torch.tensor([carry_val], dtype=cdt, device="cuda")
             got = cuda.shard_scan(xd, exclusive, carry_in=c, ws=ws)
             assert_parity(oracle, got, oracle_1d(oracle, xs, dt, exclusive, carry=carry_val), dt)
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_rows_short_and_few_long(cuda, oracle, inputs_mod, dt, exclusive):
+    """Row shapes of every row path: tiny rows (segmented warp scan, several
+    rows per warp), short rows (a warp per row), few long rows (one MCScan per
+    row); strided rows for the first two."""
+    shapes = [(1000, 1), (777, 3), (513, 17), (300, 32), (257, 33), (129, 1000), (65, 2048),
+              (33, 4095), (9, 4096), (3, (1 << 22) + 5)]
+    for R, C in shapes:
+        S = C + (16 if C < 8192 else 0)
+        x = host_input(inputs_mod, dt, R * S, seed=R * 7 + C).reshape(R, S)
+        xd = to_dev(x, dt)[:, :C]
+        got = cuda.rows(xd, exclusive=exclusive)
+        torch.cuda.synchronize()
+        xc = np.ascontiguousarray(x[:, :C])
+        if dt in ("i32", "i8"):
+            ref = oracle.rows(xc, dt, exclusive=exclusive)
+            assert np.array_equal(got.cpu().numpy(), ref), (R, C)
+        else:
+            y64, a64, _ = oracle.rows(xc, dt, exclusive=exclusive)
+            bad, worst, at = oracle.check_f32(got.cpu().numpy(), y64, a64)
+            assert bad == 0, (R, C, worst, at)
