@@ -116,6 +116,8 @@ struct McParams16 {
     int debug;
     int ahead;              // reduce jobs run this many chunks ahead of scan jobs (1..4)
     int l2;                 // L2 policies: bits 0-1 Phase-I read, bits 2-3 Phase-II re-read (0 = default)
+    int seg_tiles;          // > 0: segmented scan of contiguous rows of seg_tiles tiles (carry resets
+                            // at every row start); 0: one 1-D scan
 };
 
 template <int DT, int NC, int GPW, int NB_IN, int NB_OUT>
@@ -661,21 +663,40 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                         const int bb = lane + 32 * k;
                         rb[k] = bb < gm.g ? ld_relaxed_u64(&r_all[(int64_t)c * gm.g + bb]) : 0ull;
                     }
+                    // Segmented (rows): a block holding a row start contributes only its
+                    // sum from its last row start (Phase I), and the sums before the last
+                    // such block -- and the chunk carry -- do not reach later blocks.
+                    int lh_below = -1, lh_all = -1;
+                    if (p.seg_tiles) {
+#pragma unroll
+                        for (int k = 0; k < RPL; ++k) {
+                            const int bb = lane + 32 * k;
+                            const int u0 = c * gm.chunk_tiles + bb * gm.bt;
+                            const int u1 = u0 + gm.bt < gm.ntiles ? u0 + gm.bt : gm.ntiles;
+                            const int first = (u0 + p.seg_tiles - 1) / p.seg_tiles * p.seg_tiles;
+                            if (bb < gm.g && first < u1) {
+                                lh_all = bb;
+                                if (bb < b) lh_below = bb;
+                            }
+                        }
+                        lh_all = __reduce_max_sync(0xffffffffu, lh_all);
+                        lh_below = __reduce_max_sync(0xffffffffu, lh_below);
+                    }
                     Carry below = Carry(0), total = Carry(0);
 #pragma unroll
                     for (int k = 0; k < RPL; ++k) {
                         const int bb = lane + 32 * k;
                         const Carry v = bb < gm.g ? carry_from_bits<Carry>(rb[k]) : Carry(0);
-                        total = total + v;
-                        if (bb < b) below = below + v;
+                        if (bb >= lh_all) total = total + v;
+                        if (bb < b && bb >= lh_below) below = below + v;
                     }
                     below = warp_reduce_fixed(below);
                     total = warp_reduce_fixed(total);
                     if (lane == 0) {
-                        s_carry[c % KC] = chunk_carry + below;
+                        s_carry[c % KC] = (lh_below < 0 ? chunk_carry : Carry(0)) + below;
                         ptx::mbar_arrive(&carry_ready[c % KC]);
                     }
-                    chunk_carry = chunk_carry + total;
+                    chunk_carry = (lh_all < 0 ? chunk_carry : Carry(0)) + total;
                     ++next_car;
                     progressed = true;
                 }
@@ -725,6 +746,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 for (int t = t0; t < t1; ++t, rin.next()) {
                     mbar_wait_prof(&in_full[rin.s], rin.ph, prof0, &s_prof[1]);
                     const long long tr0 = prof ? clock64() : 0;
+                    if (p.seg_tiles && t % p.seg_tiles == 0) jsum = Carry(0);  // row start: sum from here
                     const uint8_t* slot = in_ring + rin.s * Cfg::kRingSlot;
                     if (t < gm.full_tiles) {
 #pragma unroll
@@ -765,6 +787,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     mbar_wait_prof(&in_full[s], rin.ph, prof0, &s_prof[2]);
                     const long long ts0 = prof ? clock64() : 0;
                     const bool full = t < gm.full_tiles;  // warp-uniform
+                    if (p.seg_tiles && t % p.seg_tiles == 0) carry = Carry(0);  // row start
                     int m = TILE, m_in = TILE, m_out = TILE;
                     if (!full) ragged(t, m, m_in, m_out);
                     const uint8_t* slot = in_ring + s * Cfg::kRingSlot;

@@ -231,10 +231,14 @@ struct Mc16Variant {
     using Cfg = Mc16Cfg<DT, NC, GPW, NBI, NBO>;
     static constexpr int kTile = Cfg::kTile;
 
-    static int launch(const ScanParams& sp, cudaStream_t s, const DevInfo& di, int bt, int ahead)
+    // segmented: sp's contiguous rows as one segmented scan (row length a whole
+    // number of tiles; carries reset at row starts).
+    static int launch(const ScanParams& sp, cudaStream_t s, const DevInfo& di, int bt, int ahead,
+                      bool segmented = false)
     {
         using In = typename Traits<DT>::In;
         if constexpr (Cfg::kSmem > 232448) return SCAN_ERR_ARG;  // tuning variant does not fit this dtype
+        if (segmented && sp.seg_len % kTile != 0) return SCAN_ERR_ARG;
         static std::once_flag once;
         static cudaError_t err = cudaSuccess;
         std::call_once(once, [] {
@@ -244,7 +248,7 @@ struct Mc16Variant {
         if (err != cudaSuccess) return SCAN_ERR_CUDA;
         McParams16 p;
         memset(&p, 0, sizeof(p));
-        const int64_t n = sp.seg_len;
+        const int64_t n = segmented ? sp.seg_len * sp.num_segs : sp.seg_len;
         const int64_t rows_out = n / 32;
         if (!encode_rows128(&p.tm_out, sp.out, rows_out, 4, Cfg::kBoxRowsOut)) return SCAN_ERR_CUDA;
         if constexpr (sizeof(In) == 1) {
@@ -263,6 +267,7 @@ struct Mc16Variant {
         p.debug = debug_bits();
         p.ahead = ahead < 1 ? 1 : (ahead > 4 ? 4 : ahead);
         p.l2 = env_int("SCAN_MC_L2", 0);
+        p.seg_tiles = segmented ? (int)(sp.seg_len / kTile) : 0;
         p.gm.n = n;
         p.gm.g = di.sms < kMaxGrid ? di.sms : kMaxGrid;
         const int64_t ntiles = (n + kTile - 1) / kTile;
@@ -301,7 +306,7 @@ size_t mc_workspace_bytes(int64_t n)
 // bt >= 2 tiles per block keeps the per-chunk coordination (grid barrier,
 // 148 block sums per CTA) off the critical path; ahead = 2 absorbs barrier skew.
 template <typename V, int DT>
-int launch_mc_sized(const ScanParams& p, cudaStream_t s, const DevInfo& di)
+int launch_mc_sized(const ScanParams& p, cudaStream_t s, const DevInfo& di, bool segmented = false)
 {
     using In = typename Traits<DT>::In;
     const int64_t tile_bytes = (int64_t)V::kTile * (int64_t)sizeof(In);
@@ -310,7 +315,7 @@ int launch_mc_sized(const ScanParams& p, cudaStream_t s, const DevInfo& di)
     const int64_t per_bt = (int64_t)(ahead + 1) * di.sms * tile_bytes;
     int64_t bt = (resident + per_bt / 2) / per_bt;
     bt = bt < 2 ? 2 : bt;
-    return V::launch(p, s, di, env_int("SCAN_MC_BT", (int)bt), ahead);
+    return V::launch(p, s, di, env_int("SCAN_MC_BT", (int)bt), ahead, segmented);
 }
 
 // Default variant per dtype (warps, groups per warp, input slots, output slots;
@@ -325,11 +330,44 @@ int launch_mc(const ScanParams& p, cudaStream_t s, const DevInfo& di)
         if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 2, 2, 1>, DT>(p, s, di);
         else return launch_mc_sized<Mc16Variant<DT, 16, 2, 4, 2>, DT>(p, s, di);
     case 7: return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 0>, DT>(p, s, di);   // unified in-place ring
+    case 8:
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 1, 5, 1>, DT>(p, s, di);
+        else return SCAN_ERR_ARG;
+    case 9:
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 1, 6, 1>, DT>(p, s, di);
+        else return SCAN_ERR_ARG;
+    case 10:
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 8, 2, 5, 1>, DT>(p, s, di);
+        else return SCAN_ERR_ARG;
+    case 11:
+        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 1, 4, 2>, DT>(p, s, di);
+        else return SCAN_ERR_ARG;
     default:
         if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 12, 2, 3, 1>, DT>(p, s, di);
         else if constexpr (DT == SCAN_F16_F32) return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 2>, DT>(p, s, di);
         else return launch_mc_sized<Mc16Variant<DT, 16, 2, 6, 2>, DT>(p, s, di);
     }
+}
+
+// Few long contiguous rows as ONE segmented MCScan over the whole matrix (row
+// length a multiple of the variant's tile); -1 when no variant's tile divides it.
+template <int DT>
+int launch_mc_rows(const ScanParams& p, cudaStream_t s, const DevInfo& di)
+{
+    constexpr bool wide_in = (DT == SCAN_I32_I32 || DT == SCAN_F32_F32);
+    if constexpr (wide_in) {
+        using V12 = Mc16Variant<DT, 12, 2, 3, 1>;
+        using V16 = Mc16Variant<DT, 16, 2, 2, 1>;
+        if (p.seg_len % V12::kTile == 0) return launch_mc_sized<V12, DT>(p, s, di, true);
+        if (p.seg_len % V16::kTile == 0) return launch_mc_sized<V16, DT>(p, s, di, true);
+    } else if constexpr (DT == SCAN_F16_F32) {
+        using V = Mc16Variant<DT, 16, 2, 3, 2>;
+        if (p.seg_len % V::kTile == 0) return launch_mc_sized<V, DT>(p, s, di, true);
+    } else {
+        using V = Mc16Variant<DT, 16, 2, 6, 2>;
+        if (p.seg_len % V::kTile == 0) return launch_mc_sized<V, DT>(p, s, di, true);
+    }
+    return -1;
 }
 
 // ---- batched rows of many tiles: one CTA per row (rowscan.cuh) -------------------
@@ -514,6 +552,16 @@ int launch_dt(ScanParams p, cudaStream_t s, const DevInfo& di)
         // few long rows (fewer than half the SMs, >= 2^22 elements each): one
         // full-GPU MCScan per row instead of one CTA per row -- SURVEY 8(a) a6
         const int few = env_int("SCAN_FEW_ROWS", 0);
+        // at most half as many rows as SMs (a CTA per row would leave the GPU
+        // half idle), contiguous, tile-multiple length: one segmented MCScan over
+        // all rows (the whole GPU on every row, L2 splitting intact)
+        if (p.num_segs > 1 && p.num_segs * 2 <= (int64_t)di.sms * env_int("SCAN_SEG_MC_X2", 1) &&
+            p.in_stride == p.seg_len && p.out_stride == p.seg_len && p.num_segs * p.seg_len >= kMcMinElems &&
+            p.tma_in && p.tma_out && p.row_pre == nullptr && p.carry_in == nullptr &&
+            env_int("SCAN_NO_MC", 0) == 0 && few == 0) {
+            const int st = launch_mc_rows<DT>(p, s, di);
+            if (st != -1) return st;
+        }
         if (p.num_segs > 1 && p.num_segs * 2 <= di.sms && p.seg_len >= ((int64_t)1 << 22) && p.tma_in &&
             p.tma_out && p.row_pre == nullptr && env_int("SCAN_NO_MC", 0) == 0 && few == 0) {
             using In = typename Traits<DT>::In;
