@@ -116,8 +116,8 @@ struct McParams16 {
     int debug;
     int ahead;              // reduce jobs run this many chunks ahead of scan jobs (1..4)
     int l2;                 // L2 policies: bits 0-1 Phase-I read, bits 2-3 Phase-II re-read (0 = default)
-    int seg_tiles;          // > 0: segmented scan of contiguous rows of seg_tiles tiles (carry resets
-                            // at every row start); 0: one 1-D scan
+    int64_t seg_len;        // > 0: segmented scan of contiguous rows of seg_len >= TILE elements
+                            // (carries reset at every row start); 0: one 1-D scan
 };
 
 template <int DT, int NC, int GPW, int NB_IN, int NB_OUT>
@@ -331,6 +331,40 @@ __device__ __forceinline__ void grp_emit_i8(const Grp<1>& g, uint32_t B, bool ex
     }
 }
 
+// Zero (the identity, as raw bits) the elements e0+k of a group outside [lo, hi).
+template <int SZ>
+__device__ __forceinline__ void grp_mask(Grp<SZ>& g, int e0, int lo, int hi)
+{
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int e = e0 + k;
+        if (e < lo || e >= hi) {
+            if constexpr (SZ == 4) g.w[k] = 0u;
+            else if constexpr (SZ == 2) g.w[k >> 1] &= (k & 1) ? 0x0000ffffu : 0xffff0000u;
+            else g.w[k >> 2] &= ~(0xffu << (8 * (k & 3)));
+        }
+    }
+}
+
+// Segmented scans (rows of seg_len >= TILE elements: at most one row start per
+// tile).  The tile holding the first row start at or after tile t's first
+// element (INT_MAX if that start is at or past n), and the offset of the row
+// start inside tile t.  Evaluated once per job and once per row start, so the
+// hot tile loop carries one int and one compare.
+template <int TILE>
+__device__ __forceinline__ int next_row_start_tile(int t, int64_t seg_len, int64_t n)
+{
+    const int64_t e = (int64_t)t * TILE;
+    const int64_t next = (e + seg_len - 1) / seg_len * seg_len;
+    return next < n ? (int)(next / TILE) : 0x7fffffff;
+}
+template <int TILE>
+__device__ __forceinline__ int row_start_offset(int t, int64_t seg_len)
+{
+    const int64_t e = (int64_t)t * TILE;
+    return (int)((e + seg_len - 1) / seg_len * seg_len - e);
+}
+
 // One lane's 16 elements through a tile scan: load raw words, form the lane
 // total (int8: IDP.4A byte sums; others: the in-lane inclusive prefix v), then
 // emit base + local prefix.  Used by k_mcscan16 and k_rowscan16.
@@ -445,9 +479,106 @@ __device__ __forceinline__ void store16_off(uint8_t* base, const uint32_t (&off)
     }
 }
 
-template <int DT, int NC, int GPW, int NB_IN, int NB_OUT>
+// ---- segmented scans: the tile holding a row start at offset ro > 0 -------------
+// Phase I: this lane's share of the sum of the tile's elements [ro, TILE).
+template <int DT, int GPW>
+__device__ __forceinline__ typename Traits<DT>::Carry mc_split_sum(const uint8_t* slot, const uint8_t* gin_tile, int e0_base,
+                                                                int m, int m_in, int ro)
+{
+    using Tr = Traits<DT>;
+    using Carry = typename Tr::Carry;
+    constexpr int SZ = (int)sizeof(typename Tr::In);
+    Carry sum = Carry(0);
+#pragma unroll 1
+    for (int g = 0; g < GPW; ++g) {
+        Grp<SZ> gr;
+        grp_load_tail(slot, gin_tile, e0_base + 512 * g, m, m_in, gr);
+        grp_mask(gr, e0_base + 512 * g, ro, 1 << 30);
+        sum = sum + Carry(grp_sum(gr, (const typename Tr::In*)nullptr));
+    }
+    return sum;
+}
+
+// Phase II: two masked passes over the slot -- [0, ro) with the running carry,
+// [ro, TILE) from 0 -- each a full tile scan (NC compute warps, named barrier 1,
+// s_wt[(s_count + pass) & 1]); outputs stored element-wise.  Returns the
+// aggregate of [ro, TILE), the new row's running sum.
+template <int DT, int NC, int GPW, int TILE>
+__device__ __forceinline__ typename Traits<DT>::Acc mc_split_tile(
+    const uint8_t* slot, uint8_t* ost, const uint8_t* gin_tile, typename Traits<DT>::Out* gout_tile, bool full, int m,
+    int m_in, int m_out, int ro, typename Traits<DT>::Carry carry, bool exclusive, int e0_base,
+    const LaneOffsets<(int)sizeof(typename Traits<DT>::In)> off, typename Traits<DT>::Acc* s_wt, int s_count, int lane,
+    int cw)
+{
+    using Tr = Traits<DT>;
+    using Acc = typename Tr::Acc;
+    using Carry = typename Tr::Carry;
+    using Out = typename Tr::Out;
+    constexpr int SZ = (int)sizeof(typename Tr::In);
+    constexpr uint32_t GI = LaneOffsets<SZ>::kGrpIn;
+    Acc agg = Acc(0);
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        const int lo = pass ? ro : 0, hi = pass ? TILE : ro;
+        const Carry cin = pass ? Carry(0) : carry;
+        LaneScan<DT> ls[GPW];
+        Acc ex[GPW], gp[GPW];
+        Acc wsum = Acc(0);
+#pragma unroll
+        for (int g = 0; g < GPW; ++g) {
+            if (full)
+                grp_load_off(slot + g * GI, off.in, ls[g].g);
+            else
+                grp_load_tail(slot, gin_tile, e0_base + 512 * g, m, m_in, ls[g].g);
+            grp_mask(ls[g].g, e0_base + 512 * g, lo, hi);
+            ex[g] = ls[g].prefix();
+        }
+#pragma unroll
+        for (int g = 0; g < GPW; ++g) {
+            const Acc incl = warp_incl_scan(ex[g], lane);
+            const Acc e1 = __shfl_up_sync(0xffffffffu, incl, 1);
+            ex[g] = lane == 0 ? Acc(0) : e1;
+            gp[g] = wsum;
+            wsum = wsum + __shfl_sync(0xffffffffu, incl, 31);
+        }
+        Acc* wt = s_wt + ((s_count + pass) & 1) * NC;
+        if (lane == 0) wt[cw] = wsum;
+        named_bar_sync(1, NC * 32);
+        const Acc x = lane < NC ? wt[lane] : Acc(0);
+        const Acc xi = warp_incl_scan(x, lane);
+        const Acc xe = __shfl_up_sync(0xffffffffu, xi, 1);
+        const Acc wpref = __shfl_sync(0xffffffffu, lane == 0 ? Acc(0) : xe, cw);
+        agg = __shfl_sync(0xffffffffu, xi, NC - 1);
+#pragma unroll
+        for (int g = 0; g < GPW; ++g) {
+            Acc B;
+            if constexpr (Tr::kFloat)
+                B = (float)(cin + (double)((wpref + gp[g]) + ex[g]));
+            else
+                B = cin + wpref + gp[g] + ex[g];
+            Acc o16[16];
+            ls[g].emit(B, exclusive, o16);
+            const int e0 = e0_base + 512 * g;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int e = e0 + k;
+                if (e < lo || e >= hi) continue;
+                if (e < m_out)
+                    *reinterpret_cast<Acc*>(ost + swz_elem<4>(e)) = o16[k];
+                else if (e < m)
+                    gout_tile[e] = narrow(o16[k], (Out*)nullptr);
+            }
+        }
+    }
+    return agg;
+}
+
+// SEG: segmented scan of contiguous rows (p.seg_len); a separate instantiation so
+// the 1-D kernels carry none of its code.
+template <int DT, int NC, int GPW, int NB_IN, int NB_OUT, bool SEG = false>
 __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_constant__ McParams16 p)
 {
+
     using Cfg = Mc16Cfg<DT, NC, GPW, NB_IN, NB_OUT>;
     using Tr = Traits<DT>;
     using In = typename Tr::In;
@@ -637,6 +768,12 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         // P248) -- whichever is ready first, so neither waits on the other.
         int next_pub = 0, next_car = 0;
         uint32_t backoff = 32;
+        int64_t seg_rem[SEG ? RPL : 1], seg_dc = 0;  // SEG: (start of block lane+32k of chunk next_car) mod seg_len
+        if constexpr (SEG) {
+            seg_dc = ((int64_t)gm.chunk_tiles * TILE) % p.seg_len;
+#pragma unroll
+            for (int k = 0; k < RPL; ++k) seg_rem[k] = ((int64_t)(lane + 32 * k) * gm.bt * TILE) % p.seg_len;
+        }
         long long spin0 = 0;
         while (next_car < gm.chunks) {
             bool progressed = false;
@@ -667,17 +804,21 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     // sum from its last row start (Phase I), and the sums before the last
                     // such block -- and the chunk carry -- do not reach later blocks.
                     int lh_below = -1, lh_all = -1;
-                    if (p.seg_tiles) {
+                    if constexpr (SEG) {
 #pragma unroll
                         for (int k = 0; k < RPL; ++k) {
                             const int bb = lane + 32 * k;
                             const int u0 = c * gm.chunk_tiles + bb * gm.bt;
                             const int u1 = u0 + gm.bt < gm.ntiles ? u0 + gm.bt : gm.ntiles;
-                            const int first = (u0 + p.seg_tiles - 1) / p.seg_tiles * p.seg_tiles;
-                            if (bb < gm.g && first < u1) {
+                            const int64_t e0 = (int64_t)u0 * TILE;
+                            // first row start at or after e0 (seg_rem[k] = e0 mod seg_len)
+                            const int64_t first = e0 + (seg_rem[k] == 0 ? 0 : p.seg_len - seg_rem[k]);
+                            if (bb < gm.g && u0 < u1 && first < (int64_t)u1 * TILE && first < gm.n) {
                                 lh_all = bb;
                                 if (bb < b) lh_below = bb;
                             }
+                            seg_rem[k] += seg_dc;  // the same block of the next chunk
+                            if (seg_rem[k] >= p.seg_len) seg_rem[k] -= p.seg_len;
                         }
                         lh_all = __reduce_max_sync(0xffffffffu, lh_all);
                         lh_below = __reduce_max_sync(0xffffffffu, lh_below);
@@ -743,12 +884,19 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
             if (!is_scan) {
                 // ---------------- Phase I: block reduction r[c][b] ----------------
                 Carry jsum = Carry(0);
+                int rs_tile = SEG ? next_row_start_tile<TILE>(t0, p.seg_len, gm.n) : 0x7fffffff;
                 for (int t = t0; t < t1; ++t, rin.next()) {
                     mbar_wait_prof(&in_full[rin.s], rin.ph, prof0, &s_prof[1]);
                     const long long tr0 = prof ? clock64() : 0;
-                    if (p.seg_tiles && t % p.seg_tiles == 0) jsum = Carry(0);  // row start: sum from here
                     const uint8_t* slot = in_ring + rin.s * Cfg::kRingSlot;
-                    if (t < gm.full_tiles) {
+                    if (SEG && t == rs_tile) {
+                        // a row starts in this tile: drop the sums before it (cold path)
+                        const int ro = row_start_offset<TILE>(t, p.seg_len);
+                        rs_tile = next_row_start_tile<TILE>(t + 1, p.seg_len, gm.n);
+                        int m = TILE, m_in = TILE, m_out = TILE;
+                        if (t >= gm.full_tiles) ragged(t, m, m_in, m_out);
+                        jsum = mc_split_sum<DT, GPW>(slot, gin_b + (int64_t)t * TILE * SZ, e0_base, m, m_in, ro);
+                    } else if (t < gm.full_tiles) {
 #pragma unroll
                         for (int g = 0; g < GPW; ++g) {
                             Grp<SZ> gr;
@@ -781,17 +929,37 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 // ---------------- Phase II: scan with the block carry ----------------
                 mbar_wait_prof(&carry_ready[c % KC], (uint32_t)(c / KC) & 1u, prof0, &s_prof[0]);
                 Carry carry = s_carry[c % KC];
+                int rs_tile = SEG ? next_row_start_tile<TILE>(t0, p.seg_len, gm.n) : 0x7fffffff;
                 for (int t = t0; t < t1; ++t, rin.next(), rout.next(), ++s_count) {
                     const int s = rin.s;
                     const int o = UNI ? s : rout.s;
                     mbar_wait_prof(&in_full[s], rin.ph, prof0, &s_prof[2]);
                     const long long ts0 = prof ? clock64() : 0;
                     const bool full = t < gm.full_tiles;  // warp-uniform
-                    if (p.seg_tiles && t % p.seg_tiles == 0) carry = Carry(0);  // row start
                     int m = TILE, m_in = TILE, m_out = TILE;
                     if (!full) ragged(t, m, m_in, m_out);
                     const uint8_t* slot = in_ring + s * Cfg::kRingSlot;
-
+                    int ro = 0;
+                    if (SEG && t == rs_tile) {
+                        ro = row_start_offset<TILE>(t, p.seg_len);
+                        rs_tile = next_row_start_tile<TILE>(t + 1, p.seg_len, gm.n);
+                        if (ro == 0) carry = Carry(0);  // a row starts with this tile
+                    }
+                    if (SEG && ro > 0) {
+                        // A row starts inside this tile (rare: once per row): cold path.
+                        if (!UNI && rout.wrapped) mbar_wait_prof(&out_empty[o], rout.ph ^ 1u, prof0, &s_prof[3]);
+                        const Acc agg = mc_split_tile<DT, NC, GPW, TILE>(
+                            slot, out_ring + o * Cfg::kOutSlot, gin_b + (int64_t)t * TILE * SZ, gout + (int64_t)t * TILE,
+                            full, m, m_in, m_out, ro, carry, exclusive, e0_base, off, &s_wt[0][0], s_count, lane, cw);
+                        s_count += 2;
+                        __syncwarp();
+                        if (!UNI && lane == 0) ptx::mbar_arrive(&in_empty[s]);  // both passes have read the slot
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(&store_ready[o]);
+                        carry = Carry(agg);  // the new row's running sum
+                        --s_count;           // the loop increment counts one pass
+                    } else {
                     LaneScan<DT> ls[GPW];
                     Acc ex[GPW], gp[GPW];
                     Acc wsum = Acc(0);
@@ -867,6 +1035,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                         s_prof[12] += (unsigned long long)(ts2 - ts1);
                         s_prof[13] += (unsigned long long)(te3 - ts2);
                     }
+                    }  // row start inside the tile / not
                 }
             }
         }

@@ -9,6 +9,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <type_traits>
 
 #include "../../include/scan.h"
 #include "scan_kernels.cuh"
@@ -226,23 +227,25 @@ bool encode_rows128(CUtensorMap* tm, const void* base, int64_t rows, int elem_by
 }
 
 // Second-generation MCScan: 16 contiguous elements per lane (mcscan16.cuh).
-template <int DT, int NC, int GPW, int NBI, int NBO>
+template <int DT, int NC, int GPW, int NBI, int NBO, bool SEG = false>
 struct Mc16Variant {
     using Cfg = Mc16Cfg<DT, NC, GPW, NBI, NBO>;
     static constexpr int kTile = Cfg::kTile;
 
     // segmented: sp's contiguous rows as one segmented scan (row length a whole
     // number of tiles; carries reset at row starts).
-    static int launch(const ScanParams& sp, cudaStream_t s, const DevInfo& di, int bt, int ahead,
-                      bool segmented = false)
+    static int launch(const ScanParams& sp, cudaStream_t s, const DevInfo& di, int bt, int ahead)
     {
+        constexpr bool segmented = SEG;
         using In = typename Traits<DT>::In;
         if constexpr (Cfg::kSmem > 232448) return SCAN_ERR_ARG;  // tuning variant does not fit this dtype
-        if (segmented && sp.seg_len % kTile != 0) return SCAN_ERR_ARG;
+        // segmented: rows of >= one tile (at most one row start per tile); the
+        // in-place ring would let a split tile's first pass overwrite its inputs
+        if (segmented && (sp.seg_len < kTile || Cfg::kUni)) return SCAN_ERR_ARG;
         static std::once_flag once;
         static cudaError_t err = cudaSuccess;
         std::call_once(once, [] {
-            err = cudaFuncSetAttribute(k_mcscan16<DT, NC, GPW, NBI, NBO>,
+            err = cudaFuncSetAttribute(k_mcscan16<DT, NC, GPW, NBI, NBO, SEG>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
         });
         if (err != cudaSuccess) return SCAN_ERR_CUDA;
@@ -267,7 +270,7 @@ struct Mc16Variant {
         p.debug = debug_bits();
         p.ahead = ahead < 1 ? 1 : (ahead > 4 ? 4 : ahead);
         p.l2 = env_int("SCAN_MC_L2", 0);
-        p.seg_tiles = segmented ? (int)(sp.seg_len / kTile) : 0;
+        p.seg_len = segmented ? sp.seg_len : 0;
         p.gm.n = n;
         p.gm.g = di.sms < kMaxGrid ? di.sms : kMaxGrid;
         const int64_t ntiles = (n + kTile - 1) / kTile;
@@ -283,7 +286,7 @@ struct Mc16Variant {
         p.gm.chunk_tiles = p.gm.g * p.gm.bt;
         p.gm.chunks = (int)((ntiles + p.gm.chunk_tiles - 1) / p.gm.chunk_tiles);
         void* args[] = {&p};
-        cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_mcscan16<DT, NC, GPW, NBI, NBO>,
+        cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_mcscan16<DT, NC, GPW, NBI, NBO, SEG>,
                                                     dim3(p.gm.g), dim3(Cfg::kThreads), args, Cfg::kSmem, s);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return e == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
@@ -306,7 +309,7 @@ size_t mc_workspace_bytes(int64_t n)
 // bt >= 2 tiles per block keeps the per-chunk coordination (grid barrier,
 // 148 block sums per CTA) off the critical path; ahead = 2 absorbs barrier skew.
 template <typename V, int DT>
-int launch_mc_sized(const ScanParams& p, cudaStream_t s, const DevInfo& di, bool segmented = false)
+int launch_mc_sized(const ScanParams& p, cudaStream_t s, const DevInfo& di)
 {
     using In = typename Traits<DT>::In;
     const int64_t tile_bytes = (int64_t)V::kTile * (int64_t)sizeof(In);
@@ -315,7 +318,7 @@ int launch_mc_sized(const ScanParams& p, cudaStream_t s, const DevInfo& di, bool
     const int64_t per_bt = (int64_t)(ahead + 1) * di.sms * tile_bytes;
     int64_t bt = (resident + per_bt / 2) / per_bt;
     bt = bt < 2 ? 2 : bt;
-    return V::launch(p, s, di, env_int("SCAN_MC_BT", (int)bt), ahead, segmented);
+    return V::launch(p, s, di, env_int("SCAN_MC_BT", (int)bt), ahead);
 }
 
 // Default variant per dtype (warps, groups per warp, input slots, output slots;
@@ -330,18 +333,12 @@ int launch_mc(const ScanParams& p, cudaStream_t s, const DevInfo& di)
         if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 2, 2, 1>, DT>(p, s, di);
         else return launch_mc_sized<Mc16Variant<DT, 16, 2, 4, 2>, DT>(p, s, di);
     case 7: return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 0>, DT>(p, s, di);   // unified in-place ring
-    case 8:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 1, 5, 1>, DT>(p, s, di);
-        else return SCAN_ERR_ARG;
-    case 9:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 1, 6, 1>, DT>(p, s, di);
-        else return SCAN_ERR_ARG;
-    case 10:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 8, 2, 5, 1>, DT>(p, s, di);
-        else return SCAN_ERR_ARG;
-    case 11:
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 1, 4, 2>, DT>(p, s, di);
-        else return SCAN_ERR_ARG;
+    case 20: {  // A/B: the segmented instantiation on one row
+        using V = std::conditional_t<wide_in, Mc16Variant<DT, 12, 2, 3, 1, true>,
+                                     std::conditional_t<DT == SCAN_F16_F32, Mc16Variant<DT, 16, 2, 3, 2, true>,
+                                                        Mc16Variant<DT, 16, 2, 6, 2, true>>>;
+        return launch_mc_sized<V, DT>(p, s, di);
+    }
     default:
         if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 12, 2, 3, 1>, DT>(p, s, di);
         else if constexpr (DT == SCAN_F16_F32) return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 2>, DT>(p, s, di);
@@ -349,25 +346,17 @@ int launch_mc(const ScanParams& p, cudaStream_t s, const DevInfo& di)
     }
 }
 
-// Few long contiguous rows as ONE segmented MCScan over the whole matrix (row
-// length a multiple of the variant's tile); -1 when no variant's tile divides it.
+// Few long contiguous rows as ONE segmented MCScan over the whole matrix (rows
+// of at least one tile); -1 when the rows are shorter than the variant's tile.
 template <int DT>
 int launch_mc_rows(const ScanParams& p, cudaStream_t s, const DevInfo& di)
 {
     constexpr bool wide_in = (DT == SCAN_I32_I32 || DT == SCAN_F32_F32);
-    if constexpr (wide_in) {
-        using V12 = Mc16Variant<DT, 12, 2, 3, 1>;
-        using V16 = Mc16Variant<DT, 16, 2, 2, 1>;
-        if (p.seg_len % V12::kTile == 0) return launch_mc_sized<V12, DT>(p, s, di, true);
-        if (p.seg_len % V16::kTile == 0) return launch_mc_sized<V16, DT>(p, s, di, true);
-    } else if constexpr (DT == SCAN_F16_F32) {
-        using V = Mc16Variant<DT, 16, 2, 3, 2>;
-        if (p.seg_len % V::kTile == 0) return launch_mc_sized<V, DT>(p, s, di, true);
-    } else {
-        using V = Mc16Variant<DT, 16, 2, 6, 2>;
-        if (p.seg_len % V::kTile == 0) return launch_mc_sized<V, DT>(p, s, di, true);
-    }
-    return -1;
+    using V = std::conditional_t<wide_in, Mc16Variant<DT, 12, 2, 3, 1, true>,
+                                 std::conditional_t<DT == SCAN_F16_F32, Mc16Variant<DT, 16, 2, 3, 2, true>,
+                                                    Mc16Variant<DT, 16, 2, 6, 2, true>>>;
+    if (p.seg_len < V::kTile) return -1;
+    return launch_mc_sized<V, DT>(p, s, di);
 }
 
 // ---- batched rows of many tiles: one CTA per row (rowscan.cuh) -------------------
