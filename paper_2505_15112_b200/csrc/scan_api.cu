@@ -689,7 +689,9 @@ size_t scan_workspace_bytes(int dtype, int64_t n)
 size_t scan_rows_workspace_bytes(int dtype, int64_t rows, int64_t cols)
 {
     if (!valid_dt(dtype) || rows < 0 || cols < 0) return 0;
-    return kWsDescOffset + (size_t)(rows * tiles_for(cols)) * desc_bytes(dtype);
+    const size_t lb = kWsDescOffset + (size_t)(rows * tiles_for(cols)) * desc_bytes(dtype);
+    const size_t mc = mc_workspace_bytes(rows * cols);  // few long rows: one segmented MCScan
+    return lb > mc ? lb : mc;
 }
 
 int scan_workspace_init(void* ws, size_t ws_bytes, void* stream)
