@@ -253,5 +253,180 @@ __global__ void __launch_bounds__(kThreads) k_splitw_scatter(const WParams p)
     }
 }
 
+// ---- staged split / compress: 16 elements per lane, runs written with 16-byte stores ----
+// The scatter above stores every output element on its own (2-byte stores and
+// their address arithmetic, ~45 instructions per 128 elements).  Here a warp
+// takes 16 consecutive elements per lane per step (512 per warp: one 16-byte flag
+// load, one or two 16-byte payload loads), forms the exclusive scan of the
+// per-lane true counts with a shuffle scan, and packs trues (and, for split,
+// falses -- a lane's falses before it are 16 * lane minus its trues before it)
+// into private shared-memory runs whose starts are congruent to their global
+// destinations modulo 16 bytes; every kSeg input elements the runs are written
+// with aligned 16-byte stores (element stores only for a run's first and last
+// partial vectors).  Indices (SplitInd, P283) are staged and written the same way.
+template <bool CMP, bool IDX>
+constexpr int staged_seg() { return CMP && !IDX ? 2048 : 1024; }
+constexpr int kRunPad = 32;  // >= 2 x (elements per 16-byte vector) for any payload / index run
+template <int ES, bool CMP, bool IDX>
+constexpr size_t staged_smem_bytes()
+{
+    return (size_t)kWarps * (CMP ? 1 : 2) * (staged_seg<CMP, IDX>() + kRunPad) * (ES + (IDX ? 4 : 0));
+}
+
+template <typename T, int SHIFT_MOD>
+__device__ __forceinline__ void write_run(T* __restrict__ g_aligned, const T* __restrict__ run, int shift, int cnt,
+                                          int lane)
+{
+    // run[shift, shift + cnt) -> g_aligned[shift, shift + cnt); g_aligned and run
+    // are 16-byte aligned, shift < SHIFT_MOD (a multiple of the vector length)
+    constexpr int kVecE = 16 / (int)sizeof(T);
+    const int nvec = (shift + cnt + kVecE - 1) / kVecE;
+    for (int v = lane; v < nvec; v += 32) {
+        const int lo = v * kVecE, hi = lo + kVecE;
+        if (lo >= shift && hi <= shift + cnt) {
+            *reinterpret_cast<uint4*>(g_aligned + lo) = *reinterpret_cast<const uint4*>(run + lo);
+        } else {
+            const int a0 = lo > shift ? lo : shift, a1 = hi < shift + cnt ? hi : shift + cnt;
+            for (int k = a0; k < a1; ++k) g_aligned[k] = run[k];
+        }
+    }
+}
+
+template <int ES, bool CMP, bool IDX>
+__global__ void __launch_bounds__(kThreads, 2) k_splitw_staged(const WParams p)
+{
+    using P = typename std::conditional<ES == 2, uint16_t, uint8_t>::type;
+    constexpr int kSegE = staged_seg<CMP, IDX>();
+    constexpr int kRun = kSegE + kRunPad;         // elements per staged run buffer
+    constexpr int kMod = 16 / ES;                 // run starts congruent modulo this many elements
+    static_assert(kMod % 4 == 0, "index runs (4-byte) stay 16-byte aligned under the payload's shift");
+    constexpr int kS16 = 512;                     // elements per warp step
+    constexpr int kPW = ES;                       // 16-byte payload vectors per lane per step
+    constexpr int kSegSteps = kSegE / kS16;
+    constexpr int kTileSteps = kWT / kS16;
+    constexpr int kAh = 2;                        // steps in flight
+    static_assert(kTileSteps % kSegSteps == 0 && kSegSteps % kAh == 0, "whole runs per warp tile");
+    extern __shared__ __align__(16) uint8_t s_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int gw = (blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * kThreads) >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint64_t T = reinterpret_cast<const uint64_t*>(p.hdr)[1];
+    P* const z = reinterpret_cast<P*>(p.z);
+    // per-warp runs: payload [true run][false run], then indices [true run][false run]
+    constexpr int kRuns = CMP ? 1 : 2;
+    uint8_t* const wbase = s_raw + (size_t)warp * kRuns * kRun * (ES + (IDX ? 4 : 0));
+    P* const runT = reinterpret_cast<P*>(wbase);
+    P* const runF = runT + kRun;
+    int32_t* const runTi = reinterpret_cast<int32_t*>(wbase + (size_t)kRuns * kRun * ES);
+    int32_t* const runFi = runTi + kRun;
+    for (int wt = gw; wt < p.nwt; wt += nw) {
+        const int64_t e0 = (int64_t)wt * kWT;
+        const uint64_t off = (uint64_t)__ldg(&p.cta_tot[wt / p.wpc]) + __ldg(&p.loff[wt]);
+        uint64_t tpos = off;                     // next true slot
+        uint64_t fpos = T + (uint64_t)e0 - off;  // next false slot
+        if (e0 + kWT <= p.n) {
+            const uint4* fw = reinterpret_cast<const uint4*>(p.flags + e0);
+            const uint4* pw = reinterpret_cast<const uint4*>(reinterpret_cast<const P*>(p.x) + e0);
+            uint4 fq[kAh], pq[kAh][kPW];
+#pragma unroll
+            for (int a = 0; a < kAh; ++a) {
+                fq[a] = __ldcs(fw + a * 32 + lane);
+#pragma unroll
+                for (int v = 0; v < kPW; ++v) pq[a][v] = __ldcs(pw + (a * 32 + lane) * kPW + v);
+            }
+#pragma unroll 1
+            for (int sg = 0; sg < kTileSteps; sg += kSegSteps) {
+                const int shT = (int)(tpos % kMod), shF = (int)(fpos % kMod);
+                int cT = 0;
+#pragma unroll 1
+                for (int st = sg; st < sg + kSegSteps; st += kAh) {
+#pragma unroll
+                    for (int a = 0; a < kAh; ++a) {
+                        const uint4 f = fq[a];
+                        uint32_t w[4 * kPW];
+#pragma unroll
+                        for (int v = 0; v < kPW; ++v) {
+                            w[4 * v] = pq[a][v].x; w[4 * v + 1] = pq[a][v].y;
+                            w[4 * v + 2] = pq[a][v].z; w[4 * v + 3] = pq[a][v].w;
+                        }
+                        const int nx = st + a + kAh;
+                        if (nx < kTileSteps) {
+                            fq[a] = __ldcs(fw + nx * 32 + lane);
+#pragma unroll
+                            for (int v = 0; v < kPW; ++v) pq[a][v] = __ldcs(pw + (nx * 32 + lane) * kPW + v);
+                        }
+                        const uint32_t bits = nz_bits4(f.x) | (nz_bits4(f.y) << 4) | (nz_bits4(f.z) << 8) |
+                                              (nz_bits4(f.w) << 12);
+                        const int c = __popc(bits);
+                        int incl = c;
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const int y = __shfl_up_sync(0xffffffffu, incl, d);
+                            if (lane >= d) incl += y;
+                        }
+                        const int ex = incl - c;                       // trues before this lane in the step
+                        const int sdone = (st + a - sg) * kS16;        // elements of this run's earlier steps
+                        const int tb = shT + cT + ex;                  // this lane's first true slot
+                        const int fb = shF + (sdone - cT) + (16 * lane - ex);  // ... first false slot
+                        const int32_t i0 = (int32_t)(e0 + (int64_t)(st + a) * kS16 + 16 * lane);
+                        int kt = 0, kf = 0;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            P v;
+                            if constexpr (ES == 2) v = (P)(w[j >> 1] >> (16 * (j & 1)));
+                            else v = (P)(w[j >> 2] >> (8 * (j & 3)));
+                            if ((bits >> j) & 1u) {
+                                runT[tb + kt] = v;
+                                if constexpr (IDX) runTi[tb + kt] = i0 + j;
+                                ++kt;
+                            } else if constexpr (!CMP) {
+                                runF[fb + kf] = v;
+                                if constexpr (IDX) runFi[fb + kf] = i0 + j;
+                                ++kf;
+                            }
+                        }
+                        cT += __shfl_sync(0xffffffffu, incl, 31);
+                    }
+                }
+                __syncwarp();
+                write_run<P, kMod>(z + (tpos - (uint64_t)shT), runT, shT, cT, lane);
+                if constexpr (IDX) write_run<int32_t, kMod>(p.idx_out + (tpos - (uint64_t)shT), runTi, shT, cT, lane);
+                if constexpr (!CMP) {
+                    const int cF = kSegE - cT;
+                    write_run<P, kMod>(z + (fpos - (uint64_t)shF), runF, shF, cF, lane);
+                    if constexpr (IDX)
+                        write_run<int32_t, kMod>(p.idx_out + (fpos - (uint64_t)shF), runFi, shF, cF, lane);
+                    fpos += (uint64_t)cF;
+                }
+                __syncwarp();
+                tpos += (uint64_t)cT;
+            }
+        } else {
+            // ragged last warp tile: element by element, same order
+            for (int64_t s0 = e0; s0 < p.n; s0 += 32) {
+                const int64_t e = s0 + lane;
+                const bool ok = e < p.n;
+                const bool tr = ok && p.flags[e] != 0;
+                const P val = ok ? reinterpret_cast<const P*>(p.x)[e] : (P)0;
+                const uint32_t bt = __ballot_sync(0xffffffffu, tr);
+                const uint32_t bv = __ballot_sync(0xffffffffu, ok);
+                if (tr) {
+                    const uint64_t d = tpos + __popc(bt & lt);
+                    z[d] = val;
+                    if constexpr (IDX) p.idx_out[d] = (int32_t)e;
+                } else if (ok && !CMP) {
+                    const uint64_t d = fpos + __popc(bv & ~bt & lt);
+                    z[d] = val;
+                    if constexpr (IDX) p.idx_out[d] = (int32_t)e;
+                }
+                tpos += __popc(bt);
+                fpos += __popc(bv & ~bt);
+            }
+        }
+    }
+}
+
 }  // namespace splitw
 }  // namespace scan

@@ -28,10 +28,12 @@ def _payload(n, es, seed):
 
 @pytest.mark.parametrize("es", [1, 2, 4, 8])
 @pytest.mark.parametrize("compress", [False, True])
-@pytest.mark.parametrize("kernel", ["default", "warp", "block"])
+@pytest.mark.parametrize("kernel", ["default", "warp", "direct", "block"])
 def test_split_sizes(cuda, oracle, inputs_mod, monkeypatch, es, compress, kernel):
-    if kernel != "default":  # both scatter kernels, whichever the default picks
-        monkeypatch.setenv("SCAN_SPLIT_WARP", "1" if kernel == "warp" else "0")
+    if kernel != "default":  # every scatter kernel, whichever the default picks
+        monkeypatch.setenv("SCAN_SPLIT_WARP", "0" if kernel == "block" else "1")
+    if kernel == "direct":  # the warp kernel with direct element stores instead of staged runs
+        monkeypatch.setenv("SCAN_SPLIT_DIRECT", "1")
     for n in SIZES:
         f = _flags(inputs_mod, n, seed=n)
         xd, xh = _payload(n, es, seed=n + es)
@@ -69,6 +71,26 @@ def test_split_unaligned(cuda, oracle, inputs_mod):
         zr, ir, T = oracle.split(xh[off:off + n].copy(), f[off:off + n].copy())
         assert int(cnt.item()) == T
         assert np.array_equal(z.cpu().numpy().view(np.uint16), zr) and np.array_equal(idx.cpu().numpy(), ir)
+
+
+@pytest.mark.parametrize("es", [1, 2])
+@pytest.mark.parametrize("direct", [False, True])
+def test_compress_no_indices(cuda, oracle, inputs_mod, monkeypatch, es, direct):
+    """compress without indices: the staged-run kernel (16-byte stores from a
+    per-warp run aligned to the destination) and the direct-store kernel, on the
+    recipe's mask and on all-true / all-false / sparse / alternating masks."""
+    if direct:
+        monkeypatch.setenv("SCAN_SPLIT_DIRECT", "1")
+    for n in SIZES + [3 * 4096 + 17, 8192 * 5]:
+        xd, xh = _payload(n, es, seed=n + 11 * es)
+        rng = np.random.default_rng(n)
+        masks = [_flags(inputs_mod, n, seed=n + 1), np.ones(n, np.int8), np.zeros(n, np.int8),
+                 (rng.random(n) < 0.01).astype(np.int8), (np.arange(n) % 2).astype(np.int8)]
+        for f in masks:
+            z, _, cnt = cuda.split(xd, torch.from_numpy(f).cuda(), compress=True, with_idx=False)
+            zr, _, T = oracle.split(xh, f, compress=True)
+            assert int(cnt.item()) == T
+            assert np.array_equal(z[:T].cpu().numpy().view(xh.dtype), zr), (n, es, int(f.sum()))
 
 
 def test_compress_matches_masked_select(cuda, inputs_mod):
