@@ -1,8 +1,10 @@
 """Runner for the ncu captures of the scan-application kernels
 (profiles/r01_ops_*_full.txt):
     ncu --set full -k regex:<kernel> -s 1 -c 1 python profiles/run_ops.py <op>
-op: split (2^28, fp16 payload + indices), sort (2^24 fp16 keys), top_p (1024 C4 rows, p=0.9),
-shard (C5 shard of 2^29 elements: block sums + row-kernel pass)."""
+op: split (2^28, fp16 payload + indices), compress (2^28 fp16, no indices), sort (2^24 fp16
+keys), top_p (1024 C4 rows, p=0.9), shard (C5 shard of 2^29 elements: block sums + row-kernel
+pass), rows_short (2^20 x 32 and 2^15 x 4096 fp32 rows), rows_few (8 x 2^24 fp32 rows:
+segmented MCScan)."""
 import os
 import sys
 
@@ -20,6 +22,22 @@ if op == "split":
     x = torch.randn(n, device="cuda").half()
     for _ in range(2):
         S.split(x, f)
+elif op == "compress":
+    n = 1 << 28
+    f = torch.empty(n, dtype=torch.int8, device="cuda")
+    inputs.fill_device(inputs.I8_FLAG, 2, 0, n, 0, f)
+    x = torch.randn(n, device="cuda").half()
+    for _ in range(2):
+        S.compress(x, f)
+elif op == "rows_short":
+    for R, C in ((1 << 20, 32), (1 << 15, 4096)):
+        X = torch.randn(R, C, device="cuda")
+        for _ in range(2):
+            S.rows(X)
+elif op == "rows_few":
+    X = torch.randn(8, 1 << 24, device="cuda")
+    for _ in range(2):
+        S.rows(X)
 elif op == "sort":
     k = torch.randn(1 << 24, device="cuda").half()
     for _ in range(2):
