@@ -449,7 +449,7 @@ int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t ro
     int st = dev_info(di);
     if (st != SCAN_OK) return st;
     using namespace scan::topp;
-    const size_t smem = (size_t)kCap * 8;
+    const size_t smem = kSmemBytes;
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     static int occ = 1;
@@ -460,7 +460,8 @@ int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t ro
             occ = 1;
     });
     if (err != cudaSuccess) return SCAN_ERR_CUDA;
-    const int64_t g = (int64_t)di.sms * occ < rows ? (int64_t)di.sms * occ : rows;
+    const int per_sm = env_int("SCAN_TOPP_CTAS_PER_SM", occ) < occ ? env_int("SCAN_TOPP_CTAS_PER_SM", occ) : occ;
+    const int64_t g = (int64_t)di.sms * per_sm < rows ? (int64_t)di.sms * per_sm : rows;
     k_top_p<<<(unsigned)g, scan::topp::kThreads, smem, (cudaStream_t)stream>>>(probs, rows, cols, row_stride, p, u, token_out,
                                                                     kept_out);
     g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -6,17 +6,23 @@
 // mass reaches p, draw from it.  Only the TOP of the order matters: the
 // nucleus is a prefix of the descending order, so it lies inside any set
 // {tokens with probability >= tau} whose mass reaches p.  One CTA per row:
-//   1. the row maximum m (one HBM read of the row; the row stays in L2);
-//   2. candidates {q >= tau}, tau = m * 2^-s, gathered into shared memory
-//      (warp-aggregated compaction) with their exact fp64 mass; if the mass
-//      is below p, tau is lowered (s += 8) and the row re-read from L2;
-//   3. the candidates sorted by (q descending, index ascending) -- exactly the
-//      stable descending order of the full sort -- with a bitonic network in
-//      shared memory (64-bit keys: P287's order-preserving code, ~index);
-//   4. the inclusive fp64 scan C of the sorted candidates (block scan),
-//      K = 1 + min{ j : C_j >= p }, t = u * C_{K-1}, rank = min{ k : C_k > t },
-//      token = index of rank (R15 -- the same arithmetic as the oracle, summed
-//      in a tree order instead of left to right).
+//   1. ONE read of the row: its maximum m and a candidate superset (every q
+//      within ~2^-13.25 of the running maximum, seeded from the row's first
+//      2048 elements), then per eighth-octave LEVEL l = (bits(m) - bits(q)) >> 20
+//      (monotone in q) the exact mass (u64 fixed point) and count, and the first level L
+//      whose cumulative mass reaches p.  Levels < L lie wholly inside the
+//      nucleus; the nucleus ends inside level L.
+//   2. Only level L is sorted (by q descending, index ascending -- the stable
+//      descending order of the full sort; 64-bit keys, P287's code, ~index),
+//      K = (count of levels < L) + 1 + min{ j : C_<L + C_L,j >= p }, then
+//      t = u * C_{K-1}; the draw's level l* is the first whose cumulative
+//      mass exceeds t, and only l* is sorted to find rank = min{ k : C_k > t }.
+//      Every C is an exact fp64 sum (at most 8192 fp32 terms within 2^14 of
+//      each other: 51 significant bits), so any summation order gives the
+//      oracle's left-to-right values bit for bit (R15).
+//   3. Fallbacks: a level above kLevCap elements sorts all candidates; a
+//      superset overflow or a short mass re-reads the row with candidates
+//      {q >= tau}, tau = m * 2^-s, s = 8, 12, ... (then sort + scan of all).
 // A row whose candidate set would exceed kCap before reaching mass p is not
 // handled here: token_out = -1 and the caller falls back to the sort path.
 #pragma once
@@ -28,6 +34,116 @@ namespace topp {
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
 constexpr int kCap = 8192;       // candidates per row (64 KB of 64-bit keys)
+#ifndef TOPP_UNROLL
+#define TOPP_UNROLL 4
+#endif
+constexpr int kLvlShift = 20;    // level = (bits(m) - bits(q)) >> 20: eighth octaves
+constexpr int kLevels = 106;     // levels of the one-pass candidate superset (13.25 octaves)
+constexpr int kLevCap = 2048;    // keys of one level sorted on their own
+constexpr size_t kSmemBytes = (size_t)(kCap + kLevCap) * 8;
+
+__device__ __forceinline__ double key_val(unsigned long long k)
+{
+    return (double)__uint_as_float((uint32_t)(k >> 32) & 0x7fffffffu);
+}
+
+// Bitonic sort of keys[0, n) descending (padded with 0 keys to a power of two).
+__device__ void block_sort_desc(unsigned long long* keys, int n)
+{
+    const int tid = threadIdx.x;
+    int N = 1;
+    while (N < n) N <<= 1;
+    for (int i = n + tid; i < N; i += kThreads) keys[i] = 0ull;
+    __syncthreads();
+    for (int k = 2; k <= N; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < N; i += kThreads) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const unsigned long long a = keys[i], b = keys[ixj];
+                    const bool desc = (i & k) == 0;
+                    if (desc ? (a < b) : (a > b)) {
+                        keys[i] = b;
+                        keys[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// First j in [0, n) with base + (sum of keys[0..j]) >= thr (STRICT: > thr), n if
+// none; *s_c = that prefix (valid when j < n).  Block-wide, contiguous chunks
+// per thread + fp64 block scan.
+template <bool STRICT>
+__device__ int block_first_crossing(const unsigned long long* keys, int n, double base, double thr, double* s_dred,
+                                    unsigned long long* s_min, double* s_c)
+{
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (n + kThreads - 1) / kThreads;
+    const int lo = tid * per, hi = min(n, lo + per);
+    double run = 0.0;
+    for (int i = lo; i < hi; ++i) run += key_val(keys[i]);
+    double incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    double ex = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) ex = 0.0;
+    __syncthreads();  // s_dred / s_min are free
+    if (lane == 31) s_dred[warp] = incl;
+    if (tid == 0) *s_min = (unsigned long long)n;
+    __syncthreads();
+    double wpre = 0.0;
+    for (int w = 0; w < warp; ++w) wpre += s_dred[w];
+    const double before = base + wpre + ex;
+    double c = before;
+    for (int i = lo; i < hi; ++i) {
+        c += key_val(keys[i]);
+        if (STRICT ? c > thr : c >= thr) {
+            atomicMin(s_min, (unsigned long long)i);
+            break;
+        }
+    }
+    __syncthreads();
+    const int j = (int)*s_min;
+    if (j < n && j >= lo && j < hi) {
+        double cj = before;
+        for (int i = lo; i <= j; ++i) cj += key_val(keys[i]);
+        *s_c = cj;
+    }
+    __syncthreads();
+    return j;
+}
+
+// Copy the keys[0, n) of level lvl (relative to the maximum's bits mb) to dst, in
+// any order; returns how many there are (copies at most cap).
+__device__ int block_extract_level(const unsigned long long* keys, int n, uint32_t mb, int lvl,
+                                   unsigned long long* dst, int cap, unsigned* s_ctr)
+{
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (tid == 0) *s_ctr = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < n; b0 += kThreads) {
+        const int i = b0 + tid;
+        unsigned long long key = 0ull;
+        bool take = false;
+        if (i < n) {
+            key = keys[i];
+            take = ((mb - ((uint32_t)(key >> 32) & 0x7fffffffu)) >> kLvlShift) == (uint32_t)lvl;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, take);
+        uint32_t base = 0;
+        if (lane == 0 && bal) base = atomicAdd(s_ctr, (unsigned)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0) + __popc(bal & ((1u << lane) - 1u));
+        if (take && base < (uint32_t)cap) dst[base] = key;
+    }
+    __syncthreads();
+    return (int)*s_ctr;
+}
 
 __device__ __forceinline__ float block_max(float v, float* s_red)
 {
@@ -45,32 +161,311 @@ __device__ __forceinline__ float block_max(float v, float* s_red)
 __global__ void __launch_bounds__(kThreads) k_top_p(const float* probs, int64_t rows, int64_t cols, int64_t stride,
                                                     float p, const float* u, int64_t* token_out, int32_t* kept_out)
 {
-    extern __shared__ __align__(16) unsigned long long s_key[];  // kCap sort keys
+    extern __shared__ __align__(16) unsigned long long s_key[];  // kCap candidate keys, then kLevCap level keys
+    unsigned long long* const s_lev = s_key + kCap;
     __shared__ float s_red[kWarps];
     __shared__ double s_dred[kWarps];
     __shared__ unsigned s_cnt;
+    __shared__ unsigned s_rmax;
+    __shared__ int s_level;
+    __shared__ double s_lvl[kLevels];
+    __shared__ unsigned s_lcnt[kLevels];
+    __shared__ unsigned long long s_wmass[kWarps][kLevels];  // per-warp fixed-point level masses
+    __shared__ unsigned s_wcnt[kWarps][kLevels];
+    __shared__ double s_c;
+    __shared__ double s_base;
+    __shared__ int s_aux[2];
     __shared__ unsigned long long s_min;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool vec = (cols % 4 == 0) && (stride % 4 == 0) && ((reinterpret_cast<uintptr_t>(probs) & 15) == 0);
 
     for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
         const float* q = probs + row * stride;
-        // 1. row maximum
-        float m = 0.f;
-        if (vec) {
-            for (int64_t i = tid; i < cols / 4; i += kThreads) {
-                const float4 v = __ldg(reinterpret_cast<const float4*>(q) + i);
-                m = fmaxf(m, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
-            }
-        } else {
-            for (int64_t i = tid; i < cols; i += kThreads) m = fmaxf(m, __ldg(q + i));
-        }
-        m = block_max(m, s_red);
-
-        // 2. candidates {q >= tau} until their mass reaches p
+        // 1-2 (fast path, one HBM read of the row): the row maximum and, in the same
+        // pass, a candidate SUPERSET -- every q whose bits are within 53 * 2^21 of the
+        // running block maximum's (about q >= rmax * 2^-13.25; the running maximum only
+        // grows, so this contains every q within that distance of the final m).  Then
+        // levels l = (bits(m) - bits(q)) >> 20 (eighth octaves, monotone in q), the
+        // exact fp64 mass per level (<= 8192 fp32 terms within 2^14 of each other: no
+        // rounding, any order), the smallest level L whose cumulative mass reaches p,
+        // and the candidates {l <= L} -- an upward-closed set holding the nucleus.
         int count = 0;
         bool ok = false;
-        for (int sh = 8; sh <= 160; sh += 4) {
+        float m = 0.f;
+        {
+            constexpr uint32_t kSpan = (uint32_t)kLevels << kLvlShift;
+            // seed the running maximum with the first 4 * kThreads elements' maximum
+            // (from 0, the first block-iteration would collect everything)
+            float lm = 0.f;
+            for (int64_t i = tid; i < cols && i < 4 * kThreads; i += kThreads) lm = fmaxf(lm, __ldg(q + i));
+            const float m0 = block_max(lm, s_red);
+            if (tid == 0) {
+                s_cnt = 0;
+                s_rmax = __float_as_uint(m0);
+            }
+            __syncthreads();
+            bool over = false;
+            auto collect4 = [&](int64_t i0, const float (&v)[4], int nv) {
+                const uint32_t rb = *reinterpret_cast<volatile unsigned*>(&s_rmax);
+                const uint32_t thr = rb > kSpan ? rb - kSpan : 1u;  // bits of the collection threshold (> 0)
+                uint32_t tk = 0;
+                float vm = 0.f;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (j < nv) {
+                        vm = fmaxf(vm, v[j]);
+                        if (__float_as_uint(v[j]) >= thr && v[j] > 0.f) tk |= 1u << j;
+                    }
+                }
+                lm = fmaxf(lm, vm);
+                const uint32_t wmb = __reduce_max_sync(0xffffffffu, __float_as_uint(vm));  // vm >= 0: bits order
+                if (lane == 0 && wmb > rb) atomicMax(&s_rmax, wmb);
+                const uint32_t c = __popc(tk);
+                uint32_t incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                uint32_t base = 0;
+                if (lane == 31 && incl) base = atomicAdd(&s_cnt, incl);
+                base = __shfl_sync(0xffffffffu, base, 31) + (incl - c);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if ((tk >> j) & 1u) {
+                        if (base < (unsigned)kCap) {
+                            const uint32_t code = __float_as_uint(v[j]) | 0x80000000u;
+                            s_key[base] = ((unsigned long long)code << 32) | (0xffffffffu - (uint32_t)(i0 + j));
+                        } else {
+                            over = true;
+                        }
+                        ++base;
+                    }
+                }
+            };
+            if (vec) {
+                // TOPP_UNROLL 16-byte loads in flight per thread; the values are screened
+                // together: one running-max update and (when any lane has a
+                // candidate) one warp compaction per 128 * TOPP_UNROLL elements of the warp
+                constexpr int kUnroll = TOPP_UNROLL;
+                const int64_t n4 = cols / 4;
+                for (int64_t base4 = 0; base4 < n4; base4 += kUnroll * kThreads) {
+                    float4 f[kUnroll];
+#pragma unroll
+                    for (int r = 0; r < kUnroll; ++r) {
+                        const int64_t i4 = base4 + r * kThreads + tid;
+                        f[r] = i4 < n4 ? __ldcs(reinterpret_cast<const float4*>(q) + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    const int rb = (int)*reinterpret_cast<volatile unsigned*>(&s_rmax);
+                    const int thr = rb > (int)kSpan ? rb - (int)kSpan : 1;  // bits of the threshold (> 0)
+                    float vm = 0.f;
+                    uint32_t tk = 0;
+#pragma unroll
+                    for (int r = 0; r < kUnroll; ++r) {
+                        const float v[4] = {f[r].x, f[r].y, f[r].z, f[r].w};
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            vm = fmaxf(vm, v[j]);
+                            if (__float_as_int(v[j]) >= thr) tk |= 1u << (4 * r + j);  // negative values: < 0
+                        }
+                    }
+                    lm = fmaxf(lm, vm);
+                    const uint32_t wmb = __reduce_max_sync(0xffffffffu, __float_as_uint(vm));  // vm >= 0: bits order
+                    if (lane == 0 && wmb > (uint32_t)rb) atomicMax(&s_rmax, wmb);
+                    if (__any_sync(0xffffffffu, tk != 0)) {
+                        const uint32_t c = __popc(tk);
+                        uint32_t incl = c;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                            if (lane >= o) incl += y;
+                        }
+                        uint32_t base = 0;
+                        if (lane == 31 && incl) base = atomicAdd(&s_cnt, incl);
+                        base = __shfl_sync(0xffffffffu, base, 31) + (incl - c);
+                        while (tk) {
+                            const int e = __ffs(tk) - 1;
+                            tk &= tk - 1;
+                            const int r = e >> 2, j = e & 3;
+                            float4 fr = f[0];
+#pragma unroll
+                            for (int rr = 1; rr < kUnroll; ++rr)
+                                if (rr == r) fr = f[rr];
+                            const float val = j == 0 ? fr.x : (j == 1 ? fr.y : (j == 2 ? fr.z : fr.w));
+                            const uint32_t idx = (uint32_t)((base4 + r * kThreads + tid) * 4 + j);
+                            if (base < (unsigned)kCap)
+                                s_key[base] = ((unsigned long long)(__float_as_uint(val) | 0x80000000u) << 32) |
+                                              (0xffffffffu - idx);
+                            else
+                                over = true;
+                            ++base;
+                        }
+                    }
+                }
+            } else {
+                for (int64_t b0 = 0; b0 < cols; b0 += 4 * kThreads) {
+                    const int64_t i0 = b0 + 4 * tid;
+                    float v[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) v[j] = i0 + j < cols ? __ldg(q + i0 + j) : 0.f;
+                    const int64_t rem = cols - i0;
+                    collect4(i0, v, rem <= 0 ? 0 : (rem > 4 ? 4 : (int)rem));
+                }
+            }
+            m = block_max(lm, s_red);
+            over = __syncthreads_or(over);
+            count = (int)s_cnt;
+            if (!over && (__float_as_uint(m) >> 23) >= 15u) {  // fixed-point levels need E_m - 14 >= 1
+                const uint32_t mb = __float_as_uint(m);
+                // level masses in fixed point: q = mant * 2^(E_q - 150) with E_q >= E_m - 14
+                // for every level, so q / 2^(E_m - 164) = mant << (E_q - E_m + 14) < 2^38 is an
+                // integer and <= 8192 of them sum below 2^51: exact u64 (per-warp bins, no fp
+                // atomics), then one exact conversion per level
+                const int Em = (int)(mb >> 23);
+                for (int i = tid; i < kWarps * kLevels; i += kThreads) {
+                    (&s_wmass[0][0])[i] = 0ull;
+                    (&s_wcnt[0][0])[i] = 0u;
+                }
+                __syncthreads();
+                for (int i = tid; i < count; i += kThreads) {
+                    const uint32_t code = (uint32_t)(s_key[i] >> 32) & 0x7fffffffu;
+                    const uint32_t d = mb - code;  // code <= mb
+                    if (d < kSpan) {
+                        const int Eq = (int)(code >> 23);
+                        const unsigned long long fx = (unsigned long long)((code & 0x7fffffu) | 0x800000u)
+                                                      << (Eq - Em + 14);
+                        atomicAdd(&s_wmass[warp][d >> kLvlShift], fx);
+                        atomicAdd(&s_wcnt[warp][d >> kLvlShift], 1u);
+                    }
+                }
+                __syncthreads();
+                for (int l = tid; l < kLevels; l += kThreads) {
+                    unsigned long long sm = 0ull;
+                    unsigned c = 0u;
+                    for (int w = 0; w < kWarps; ++w) {
+                        sm += s_wmass[w][l];
+                        c += s_wcnt[w][l];
+                    }
+                    s_lvl[l] = ldexp((double)sm, Em - 164);
+                    s_lcnt[l] = c;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    double cum = 0.0;
+                    int L = -1;
+                    for (int l = 0; l < kLevels; ++l) {
+                        cum += s_lvl[l];
+                        if (cum >= (double)p) {
+                            L = l;
+                            break;
+                        }
+                    }
+                    s_level = L;
+                }
+                __syncthreads();
+                const int L = s_level;
+                if (L >= 0 && s_lcnt[L] <= (unsigned)kLevCap) {
+                    // ---- level path: sort level L only (and the draw's level) ----
+                    if (tid == 0) {
+                        double base = 0.0;
+                        unsigned nb = 0;
+                        for (int l = 0; l < L; ++l) {
+                            base += s_lvl[l];
+                            nb += s_lcnt[l];
+                        }
+                        s_base = base;
+                        s_aux[0] = (int)nb;
+                    }
+                    const int nL = block_extract_level(s_key, count, mb, L, s_lev, kLevCap, &s_cnt);
+                    const double baseL = s_base;
+                    const int nbefL = s_aux[0];
+                    block_sort_desc(s_lev, nL);
+                    const int jL = block_first_crossing<false>(s_lev, nL, baseL, (double)p, s_dred, &s_min, &s_c);
+                    if (jL < nL) {  // always: cum(<= L) >= p
+                        const int K = nbefL + jL + 1;
+                        const double CK = s_c;
+                        const double t = (double)__ldg(u + row) * CK;
+                        if (tid == 0) {
+                            double cum = 0.0;
+                            int ls = L;
+                            unsigned nb = 0;
+                            for (int l = 0; l < L; ++l) {
+                                if (cum + s_lvl[l] > t) {
+                                    ls = l;
+                                    break;
+                                }
+                                cum += s_lvl[l];
+                                nb += s_lcnt[l];
+                            }
+                            s_base = cum;
+                            s_aux[1] = ls;
+                        }
+                        __syncthreads();
+                        const int ls = s_aux[1];
+                        const double base2 = s_base;
+                        int nl = jL + 1;  // level L: only its nucleus part
+                        bool lev_ok = true;
+                        if (ls != L) {
+                            if (s_lcnt[ls] <= (unsigned)kLevCap) {
+                                nl = block_extract_level(s_key, count, mb, ls, s_lev, kLevCap, &s_cnt);
+                                block_sort_desc(s_lev, nl);
+                            } else {
+                                lev_ok = false;
+                            }
+                        }
+                        if (lev_ok) {
+                            int r = block_first_crossing<true>(s_lev, nl, ls == L ? baseL : base2, t, s_dred, &s_min,
+                                                               &s_c);
+                            if (r >= nl) r = nl - 1;  // t within rounding of the level's end: its last element
+                            if (tid == 0) {
+                                token_out[row] = (int64_t)(0xffffffffu - (uint32_t)(s_lev[r] & 0xffffffffu));
+                                if (kept_out) kept_out[row] = K;
+                            }
+                            __syncthreads();
+                            continue;  // next row
+                        }
+                    }
+                }
+                if (L >= 0) {
+                    // keep {level <= L}: read this thread's contiguous share, then write
+                    constexpr int kPer = kCap / kThreads;
+                    const int lo = tid * kPer, hi = min(count, lo + kPer);
+                    unsigned long long key[kPer];
+                    uint32_t keep = 0;  // bit k: key[k] is kept (static indices: registers)
+#pragma unroll
+                    for (int k = 0; k < kPer; ++k) {
+                        key[k] = lo + k < hi ? s_key[lo + k] : 0ull;
+                        const uint32_t code = (uint32_t)(key[k] >> 32) & 0x7fffffffu;
+                        if (lo + k < hi && ((mb - code) >> kLvlShift) <= (uint32_t)L) keep |= 1u << k;
+                    }
+                    const int nk = __popc(keep);
+                    int incl = nk;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += y;
+                    }
+                    if (lane == 31) s_red[warp] = __int_as_float(incl);
+                    __syncthreads();
+                    int wpre = 0, tot = 0;
+                    for (int w = 0; w < kWarps; ++w) {
+                        const int y = __float_as_int(s_red[w]);
+                        if (w < warp) wpre += y;
+                        tot += y;
+                    }
+                    int ob = wpre + incl - nk;
+#pragma unroll
+                    for (int k = 0; k < kPer; ++k)
+                        if ((keep >> k) & 1u) s_key[ob++] = key[k];
+                    count = tot;
+                    ok = true;
+                    __syncthreads();
+                }
+            }
+        }
+
+        // 1-2 (fallback): candidates {q >= tau} until their mass reaches p
+        for (int sh = 8; !ok && sh <= 160; sh += 4) {
             const float tau = sh >= 150 ? 0.f : ldexpf(m, -sh);
             if (tid == 0) s_cnt = 0;
             __syncthreads();
@@ -149,86 +544,28 @@ __global__ void __launch_bounds__(kThreads) k_top_p(const float* probs, int64_t 
             continue;
         }
 
-        // 3. bitonic sort, descending by (code, ~index), padded to a power of two
-        int N = 1;
-        while (N < count) N <<= 1;
-        for (int i = count + tid; i < N; i += kThreads) s_key[i] = 0ull;
-        __syncthreads();
-        for (int k = 2; k <= N; k <<= 1) {
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = tid; i < N; i += kThreads) {
-                    const int ixj = i ^ j;
-                    if (ixj > i) {
-                        const unsigned long long a = s_key[i], b = s_key[ixj];
-                        const bool desc = (i & k) == 0;
-                        if (desc ? (a < b) : (a > b)) {
-                            s_key[i] = b;
-                            s_key[ixj] = a;
-                        }
-                    }
-                }
-                __syncthreads();
+        // 3. all candidates sorted, descending by (code, ~index)
+        block_sort_desc(s_key, count);
+        // 4. K = 1 + min{ j : C_j >= p }, t = u * C_{K-1}, rank = min{ k : C_k > t }
+        const int jK = block_first_crossing<false>(s_key, count, 0.0, (double)p, s_dred, &s_min, &s_c);
+        int K = count;
+        double CK = 0.0;
+        if (jK < count) {
+            K = jK + 1;
+            CK = s_c;
+        } else {  // the candidates' whole mass is below p (tau = 0: the whole row)
+            if (tid == 0) {
+                double c = 0.0;
+                for (int i = 0; i < count; ++i) c += key_val(s_key[i]);
+                s_c = c;
             }
+            __syncthreads();
+            CK = s_c;
         }
-
-        // 4. inclusive fp64 scan over the sorted candidates; nucleus; draw
-        const int per = (count + kThreads - 1) / kThreads;  // consecutive elements per thread
-        const int lo = tid * per, hi = min(count, lo + per);
-        double run = 0.0;
-        for (int i = lo; i < hi; ++i) run += (double)__uint_as_float((uint32_t)(s_key[i] >> 32) & 0x7fffffffu);
-        double incl = run;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const double y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) s_dred[warp] = incl;
-        __syncthreads();
-        double wpre = 0.0;
-        for (int w = 0; w < warp; ++w) wpre += s_dred[w];
-        double ex = __shfl_up_sync(0xffffffffu, incl, 1);
-        if (lane == 0) ex = 0.0;
-        const double before = wpre + ex;  // exclusive prefix of this thread's first element
-        // K = 1 + min{ j : C_j >= p }
-        if (tid == 0) s_min = (unsigned long long)count;
-        __syncthreads();
-        {
-            double c = before;
-            for (int i = lo; i < hi; ++i) {
-                c += (double)__uint_as_float((uint32_t)(s_key[i] >> 32) & 0x7fffffffu);
-                if (c >= (double)p) {
-                    atomicMin(&s_min, (unsigned long long)i);
-                    break;
-                }
-            }
-        }
-        __syncthreads();
-        const int jK = (int)s_min;
-        const int K = jK < count ? jK + 1 : count;
-        __syncthreads();
-        // C_{K-1}: the thread owning K-1 publishes it
-        if (K - 1 >= lo && K - 1 < hi) {
-            double c = before;
-            for (int i = lo; i <= K - 1; ++i) c += (double)__uint_as_float((uint32_t)(s_key[i] >> 32) & 0x7fffffffu);
-            s_dred[0] = c;
-        }
-        if (tid == 0) s_min = (unsigned long long)K;
-        __syncthreads();
-        const double t = (double)__ldg(u + row) * s_dred[0];
-        {
-            double c = before;
-            for (int i = lo; i < hi && i < K; ++i) {
-                c += (double)__uint_as_float((uint32_t)(s_key[i] >> 32) & 0x7fffffffu);
-                if (c > t) {
-                    atomicMin(&s_min, (unsigned long long)i);
-                    break;
-                }
-            }
-        }
-        __syncthreads();
+        const double t = (double)__ldg(u + row) * CK;
+        int r = block_first_crossing<true>(s_key, K, 0.0, t, s_dred, &s_min, &s_c);
+        if (r >= K) r = K - 1;
         if (tid == 0) {
-            int r = (int)s_min;
-            if (r >= K) r = K - 1;
             token_out[row] = (int64_t)(0xffffffffu - (uint32_t)(s_key[r] & 0xffffffffu));
             if (kept_out) kept_out[row] = K;
         }
