@@ -129,15 +129,16 @@ int launch_split_warp(const SplitParams& sp, cudaStream_t s, const DevInfo& di)
     k_splitw_count<<<(unsigned)grid, kThreads, 0, s>>>(p);
     const int64_t want = ((int64_t)p.nwt + kWarps - 1) / kWarps;
     const int64_t g2 = (int64_t)di.sms * 4 < want ? (int64_t)di.sms * 4 : want;
-    auto staged = [&](auto kern, size_t smem) -> int {
-        // staged runs + 16-byte stores; 1-2 CTAs per SM by shared memory
+    auto staged = [&](auto kern, size_t smem, int nt) -> int {
+        // staged runs + 16-byte stores; CTAs per SM by shared memory
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return SCAN_ERR_CUDA;
         int occ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem) != cudaSuccess || occ < 1)
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, nt, smem) != cudaSuccess || occ < 1)
             return SCAN_ERR_CUDA;
-        const int64_t g3 = (int64_t)di.sms * occ < want ? (int64_t)di.sms * occ : want;
-        kern<<<(unsigned)g3, kThreads, smem, s>>>(p);
+        const int64_t wantc = ((int64_t)p.nwt + nt / 32 - 1) / (nt / 32);
+        const int64_t g3 = (int64_t)di.sms * occ < wantc ? (int64_t)di.sms * occ : wantc;
+        kern<<<(unsigned)g3, nt, smem, s>>>(p);
         return SCAN_OK;
     };
     const bool direct = getenv("SCAN_SPLIT_DIRECT") != nullptr;
@@ -147,18 +148,18 @@ int launch_split_warp(const SplitParams& sp, cudaStream_t s, const DevInfo& di)
             if (p.idx_out) k_splitw_scatter<ES, true, true><<<(unsigned)g2, kThreads, 0, s>>>(p);
             else k_splitw_scatter<ES, true, false><<<(unsigned)g2, kThreads, 0, s>>>(p);
         } else if (p.idx_out) {
-            st = staged(k_splitw_staged<ES, true, true>, staged_smem_bytes<ES, true, true>());
+            st = staged(k_splitw_staged<ES, true, true, 256>, staged_smem_bytes<ES, true, true, 256>(), 256);
         } else {
-            st = staged(k_splitw_staged<ES, true, false>, staged_smem_bytes<ES, true, false>());
+            st = staged(k_splitw_staged<ES, true, false>, staged_smem_bytes<ES, true, false>(), kThreads);
         }
     } else {
         if (direct) {
             if (p.idx_out) k_splitw_scatter<ES, false, true><<<(unsigned)g2, kThreads, 0, s>>>(p);
             else k_splitw_scatter<ES, false, false><<<(unsigned)g2, kThreads, 0, s>>>(p);
         } else if (p.idx_out) {
-            st = staged(k_splitw_staged<ES, false, true>, staged_smem_bytes<ES, false, true>());
+            st = staged(k_splitw_staged<ES, false, true, 256>, staged_smem_bytes<ES, false, true, 256>(), 256);
         } else {
-            st = staged(k_splitw_staged<ES, false, false>, staged_smem_bytes<ES, false, false>());
+            st = staged(k_splitw_staged<ES, false, false, 256>, staged_smem_bytes<ES, false, false, 256>(), 256);
         }
     }
     if (st != SCAN_OK) return st;

@@ -264,13 +264,41 @@ __global__ void __launch_bounds__(kThreads) k_splitw_scatter(const WParams p)
 // destinations modulo 16 bytes; every kSeg input elements the runs are written
 // with aligned 16-byte stores (element stores only for a run's first and last
 // partial vectors).  Indices (SplitInd, P283) are staged and written the same way.
+#ifndef SPLIT_IDX_SEG
+#define SPLIT_IDX_SEG 512
+#endif
 template <bool CMP, bool IDX>
-constexpr int staged_seg() { return CMP && !IDX ? 2048 : 1024; }
+constexpr int staged_seg() { return CMP && !IDX ? 2048 : (!CMP && IDX ? SPLIT_IDX_SEG : 1024); }
 constexpr int kRunPad = 32;  // >= 2 x (elements per 16-byte vector) for any payload / index run
-template <int ES, bool CMP, bool IDX>
+// per warp: the payload run(s), then the index run(s) as 16-bit positions in the warp tile
+template <int ES, bool CMP, bool IDX, int NT = kThreads>
 constexpr size_t staged_smem_bytes()
 {
-    return (size_t)kWarps * (CMP ? 1 : 2) * (staged_seg<CMP, IDX>() + kRunPad) * (ES + (IDX ? 4 : 0));
+    return (size_t)(NT / 32) * (CMP ? 1 : 2) * (staged_seg<CMP, IDX>() + kRunPad) * (ES + (IDX ? 2 : 0));
+}
+
+// run[shift, shift + cnt) of 16-bit warp-tile positions -> g_aligned[k] = base + run[k]
+// (int32 indices), 16-byte stores of 4 indices; shift is the payload's (a multiple of 4
+// keeps g_aligned 16-byte aligned)
+__device__ __forceinline__ void write_idx_run(int32_t* __restrict__ g_aligned, const uint16_t* __restrict__ run,
+                                              int shift, int cnt, int32_t base, int lane)
+{
+    const int nvec = (shift + cnt + 3) / 4;
+    for (int v = lane; v < nvec; v += 32) {
+        const int lo = v * 4, hi = lo + 4;
+        if (lo >= shift && hi <= shift + cnt) {
+            const uint2 w = *reinterpret_cast<const uint2*>(run + lo);
+            int4 o;
+            o.x = base + (int32_t)(w.x & 0xffffu);
+            o.y = base + (int32_t)(w.x >> 16);
+            o.z = base + (int32_t)(w.y & 0xffffu);
+            o.w = base + (int32_t)(w.y >> 16);
+            *reinterpret_cast<int4*>(g_aligned + lo) = o;
+        } else {
+            const int a0 = lo > shift ? lo : shift, a1 = hi < shift + cnt ? hi : shift + cnt;
+            for (int k = a0; k < a1; ++k) g_aligned[k] = base + (int32_t)run[k];
+        }
+    }
 }
 
 template <typename T, int SHIFT_MOD>
@@ -292,8 +320,8 @@ __device__ __forceinline__ void write_run(T* __restrict__ g_aligned, const T* __
     }
 }
 
-template <int ES, bool CMP, bool IDX>
-__global__ void __launch_bounds__(kThreads, 2) k_splitw_staged(const WParams p)
+template <int ES, bool CMP, bool IDX, int NT = kThreads>
+__global__ void __launch_bounds__(NT, 1024 / NT) k_splitw_staged(const WParams p)
 {
     using P = typename std::conditional<ES == 2, uint16_t, uint8_t>::type;
     constexpr int kSegE = staged_seg<CMP, IDX>();
@@ -304,23 +332,23 @@ __global__ void __launch_bounds__(kThreads, 2) k_splitw_staged(const WParams p)
     constexpr int kPW = ES;                       // 16-byte payload vectors per lane per step
     constexpr int kSegSteps = kSegE / kS16;
     constexpr int kTileSteps = kWT / kS16;
-    constexpr int kAh = 2;                        // steps in flight
-    static_assert(kTileSteps % kSegSteps == 0 && kSegSteps % kAh == 0, "whole runs per warp tile");
+    constexpr int kAh = 2;                        // steps in flight (runs may be shorter: written mid-loop)
+    static_assert(kTileSteps % kSegSteps == 0 && kTileSteps % kAh == 0, "whole runs and prefetch groups per tile");
     extern __shared__ __align__(16) uint8_t s_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int gw = (blockIdx.x * kThreads + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * kThreads) >> 5;
+    const int gw = (blockIdx.x * NT + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * NT) >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const uint64_t T = reinterpret_cast<const uint64_t*>(p.hdr)[1];
     P* const z = reinterpret_cast<P*>(p.z);
     // per-warp runs: payload [true run][false run], then indices [true run][false run]
     constexpr int kRuns = CMP ? 1 : 2;
-    uint8_t* const wbase = s_raw + (size_t)warp * kRuns * kRun * (ES + (IDX ? 4 : 0));
+    uint8_t* const wbase = s_raw + (size_t)warp * kRuns * kRun * (ES + (IDX ? 2 : 0));
     P* const runT = reinterpret_cast<P*>(wbase);
     P* const runF = runT + kRun;
-    int32_t* const runTi = reinterpret_cast<int32_t*>(wbase + (size_t)kRuns * kRun * ES);
-    int32_t* const runFi = runTi + kRun;
+    uint16_t* const runTi = reinterpret_cast<uint16_t*>(wbase + (size_t)kRuns * kRun * ES);  // positions in the tile
+    uint16_t* const runFi = runTi + kRun;
     for (int wt = gw; wt < p.nwt; wt += nw) {
         const int64_t e0 = (int64_t)wt * kWT;
         const uint64_t off = (uint64_t)__ldg(&p.cta_tot[wt / p.wpc]) + __ldg(&p.loff[wt]);
@@ -336,72 +364,77 @@ __global__ void __launch_bounds__(kThreads, 2) k_splitw_staged(const WParams p)
 #pragma unroll
                 for (int v = 0; v < kPW; ++v) pq[a][v] = __ldcs(pw + (a * 32 + lane) * kPW + v);
             }
+            int shT = (int)(tpos % kMod), shF = (int)(fpos % kMod);
+            int cT = 0, sdone = 0;  // trues / elements of the current run so far
 #pragma unroll 1
-            for (int sg = 0; sg < kTileSteps; sg += kSegSteps) {
-                const int shT = (int)(tpos % kMod), shF = (int)(fpos % kMod);
-                int cT = 0;
-#pragma unroll 1
-                for (int st = sg; st < sg + kSegSteps; st += kAh) {
+            for (int st0 = 0; st0 < kTileSteps; st0 += kAh) {
 #pragma unroll
-                    for (int a = 0; a < kAh; ++a) {
-                        const uint4 f = fq[a];
-                        uint32_t w[4 * kPW];
+                for (int a = 0; a < kAh; ++a) {
+                    const int st = st0 + a;
+                    const uint4 f = fq[a];
+                    uint32_t w[4 * kPW];
 #pragma unroll
-                        for (int v = 0; v < kPW; ++v) {
-                            w[4 * v] = pq[a][v].x; w[4 * v + 1] = pq[a][v].y;
-                            w[4 * v + 2] = pq[a][v].z; w[4 * v + 3] = pq[a][v].w;
+                    for (int v = 0; v < kPW; ++v) {
+                        w[4 * v] = pq[a][v].x; w[4 * v + 1] = pq[a][v].y;
+                        w[4 * v + 2] = pq[a][v].z; w[4 * v + 3] = pq[a][v].w;
+                    }
+                    const int nx = st + kAh;
+                    if (nx < kTileSteps) {
+                        fq[a] = __ldcs(fw + nx * 32 + lane);
+#pragma unroll
+                        for (int v = 0; v < kPW; ++v) pq[a][v] = __ldcs(pw + (nx * 32 + lane) * kPW + v);
+                    }
+                    const uint32_t bits = nz_bits4(f.x) | (nz_bits4(f.y) << 4) | (nz_bits4(f.z) << 8) |
+                                          (nz_bits4(f.w) << 12);
+                    const int c = __popc(bits);
+                    int incl = c;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, incl, d);
+                        if (lane >= d) incl += y;
+                    }
+                    const int ex = incl - c;                               // trues before this lane in the step
+                    const int tb = shT + cT + ex;                          // this lane's first true slot
+                    const int fb = shF + (sdone - cT) + (16 * lane - ex);  // ... first false slot
+                    const int i0 = st * kS16 + 16 * lane;                  // position in the warp tile
+                    int kt = 0, kf = 0;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        P v;
+                        if constexpr (ES == 2) v = (P)(w[j >> 1] >> (16 * (j & 1)));
+                        else v = (P)(w[j >> 2] >> (8 * (j & 3)));
+                        if ((bits >> j) & 1u) {
+                            runT[tb + kt] = v;
+                            if constexpr (IDX) runTi[tb + kt] = (uint16_t)(i0 + j);
+                            ++kt;
+                        } else if constexpr (!CMP) {
+                            runF[fb + kf] = v;
+                            if constexpr (IDX) runFi[fb + kf] = (uint16_t)(i0 + j);
+                            ++kf;
                         }
-                        const int nx = st + a + kAh;
-                        if (nx < kTileSteps) {
-                            fq[a] = __ldcs(fw + nx * 32 + lane);
-#pragma unroll
-                            for (int v = 0; v < kPW; ++v) pq[a][v] = __ldcs(pw + (nx * 32 + lane) * kPW + v);
+                    }
+                    cT += __shfl_sync(0xffffffffu, incl, 31);
+                    sdone += kS16;
+                    if (sdone == kSegE) {  // the run is complete: write it, start the next
+                        __syncwarp();
+                        write_run<P, kMod>(z + (tpos - (uint64_t)shT), runT, shT, cT, lane);
+                        if constexpr (IDX)
+                            write_idx_run(p.idx_out + (tpos - (uint64_t)shT), runTi, shT, cT, (int32_t)e0, lane);
+                        if constexpr (!CMP) {
+                            const int cF = kSegE - cT;
+                            write_run<P, kMod>(z + (fpos - (uint64_t)shF), runF, shF, cF, lane);
+                            if constexpr (IDX)
+                                write_idx_run(p.idx_out + (fpos - (uint64_t)shF), runFi, shF, cF, (int32_t)e0, lane);
+                            fpos += (uint64_t)cF;
                         }
-                        const uint32_t bits = nz_bits4(f.x) | (nz_bits4(f.y) << 4) | (nz_bits4(f.z) << 8) |
-                                              (nz_bits4(f.w) << 12);
-                        const int c = __popc(bits);
-                        int incl = c;
-#pragma unroll
-                        for (int d = 1; d < 32; d <<= 1) {
-                            const int y = __shfl_up_sync(0xffffffffu, incl, d);
-                            if (lane >= d) incl += y;
-                        }
-                        const int ex = incl - c;                       // trues before this lane in the step
-                        const int sdone = (st + a - sg) * kS16;        // elements of this run's earlier steps
-                        const int tb = shT + cT + ex;                  // this lane's first true slot
-                        const int fb = shF + (sdone - cT) + (16 * lane - ex);  // ... first false slot
-                        const int32_t i0 = (int32_t)(e0 + (int64_t)(st + a) * kS16 + 16 * lane);
-                        int kt = 0, kf = 0;
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            P v;
-                            if constexpr (ES == 2) v = (P)(w[j >> 1] >> (16 * (j & 1)));
-                            else v = (P)(w[j >> 2] >> (8 * (j & 3)));
-                            if ((bits >> j) & 1u) {
-                                runT[tb + kt] = v;
-                                if constexpr (IDX) runTi[tb + kt] = i0 + j;
-                                ++kt;
-                            } else if constexpr (!CMP) {
-                                runF[fb + kf] = v;
-                                if constexpr (IDX) runFi[fb + kf] = i0 + j;
-                                ++kf;
-                            }
-                        }
-                        cT += __shfl_sync(0xffffffffu, incl, 31);
+                        __syncwarp();
+                        tpos += (uint64_t)cT;
+                        shT = (int)(tpos % kMod);
+                        shF = (int)(fpos % kMod);
+                        cT = 0;
+                        sdone = 0;
                     }
                 }
-                __syncwarp();
-                write_run<P, kMod>(z + (tpos - (uint64_t)shT), runT, shT, cT, lane);
-                if constexpr (IDX) write_run<int32_t, kMod>(p.idx_out + (tpos - (uint64_t)shT), runTi, shT, cT, lane);
-                if constexpr (!CMP) {
-                    const int cF = kSegE - cT;
-                    write_run<P, kMod>(z + (fpos - (uint64_t)shF), runF, shF, cF, lane);
-                    if constexpr (IDX)
-                        write_run<int32_t, kMod>(p.idx_out + (fpos - (uint64_t)shF), runFi, shF, cF, lane);
-                    fpos += (uint64_t)cF;
-                }
-                __syncwarp();
-                tpos += (uint64_t)cT;
             }
         } else {
             // ragged last warp tile: element by element, same order
