@@ -25,6 +25,8 @@ namespace {
 
 std::atomic<uint64_t> g_launches{0};
 
+int env_int(const char* name, int dflt);  // tuning / A-B knobs (below)
+
 // Smallest tile any variant uses: workspaces are sized for it so a workspace
 // fits every variant (kernel variants are selectable for tuning).
 constexpr int64_t kMinTile = 4096;
@@ -122,13 +124,18 @@ struct Variant {
         cfg.blockDim = dim3(TH);
         cfg.dynamicSmemBytes = kSmem;
         cfg.stream = s;
-        cudaLaunchAttribute attr[1];
+        cudaLaunchAttribute attr[2];
         attr[0].id = cudaLaunchAttributeClusterDimension;
         attr[0].val.clusterDim.x = (unsigned)p.num_tiles;
         attr[0].val.clusterDim.y = 1;
         attr[0].val.clusterDim.z = 1;
+        // programmatic dependent launch: this (latency-bound) launch overlaps the
+        // tail of the previous kernel in the stream; the kernel waits for it
+        // (griddepcontrol.wait) before touching global memory
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 1;
+        cfg.numAttrs = env_int("SCAN_PDL", 1) ? 2 : 1;
         cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return e == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
@@ -145,6 +152,23 @@ struct Variant {
         p.debug = debug_bits();
         int64_t grid = (int64_t)di.sms * occ;
         if (grid > p.num_tiles) grid = p.num_tiles;
+        if (grid <= di.sms && env_int("SCAN_PDL", 1)) {
+            // one wave of a latency-bound launch: programmatic dependent launch, as
+            // for the cluster path (the kernel waits before touching global memory)
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)grid);
+            cfg.blockDim = dim3(TH);
+            cfg.dynamicSmemBytes = kSmem;
+            cfg.stream = s;
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[0].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            const cudaError_t e = cudaLaunchKernelEx(&cfg, k_scan_tiles<DT, TH, RW, ST, OS, MB>, p);
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            return e == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+        }
         k_scan_tiles<DT, TH, RW, ST, OS, MB><<<(unsigned)grid, TH, kSmem, s>>>(p);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;

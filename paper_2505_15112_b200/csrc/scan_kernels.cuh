@@ -476,13 +476,20 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
         s_tma[s] = tma;
     };
 
+    // Programmatic dependent launch (cluster launches of small n): the next kernel
+    // in the stream may start launching now; it waits in ITS griddepcontrol.wait
+    // until this grid has completed and flushed.  No-ops without the attribute.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&full_bar[s], 1);
+        ptx::fence_mbar_init();
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the previous kernel's writes are visible
     if (tid == 0) {
         if (!p.static_sched) {
             if (hdr->magic != kWsMagic) hdr->error = 1;
             s_epoch = hdr->epoch;
         }
-        for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&full_bar[s], 1);
-        ptx::fence_mbar_init();
         for (int s = 0; s < STAGES; ++s) issue(s, s);
     }
     __syncthreads();
