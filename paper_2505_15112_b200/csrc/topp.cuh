@@ -249,12 +249,21 @@ __global__ void __launch_bounds__(kThreads) k_top_p(const float* probs, int64_t 
                 // candidate) one warp compaction per 128 * TOPP_UNROLL elements of the warp
                 constexpr int kUnroll = TOPP_UNROLL;
                 const int64_t n4 = cols / 4;
+                // software-pipelined: the next iteration's loads are issued before this
+                // iteration's values are screened
+                float4 nf[kUnroll];
+#pragma unroll
+                for (int r = 0; r < kUnroll; ++r) {
+                    const int64_t i4 = (int64_t)r * kThreads + tid;
+                    nf[r] = i4 < n4 ? __ldcs(reinterpret_cast<const float4*>(q) + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
                 for (int64_t base4 = 0; base4 < n4; base4 += kUnroll * kThreads) {
                     float4 f[kUnroll];
 #pragma unroll
                     for (int r = 0; r < kUnroll; ++r) {
-                        const int64_t i4 = base4 + r * kThreads + tid;
-                        f[r] = i4 < n4 ? __ldcs(reinterpret_cast<const float4*>(q) + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        f[r] = nf[r];
+                        const int64_t i4 = base4 + kUnroll * kThreads + r * kThreads + tid;
+                        nf[r] = i4 < n4 ? __ldcs(reinterpret_cast<const float4*>(q) + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
                     const int rb = (int)*reinterpret_cast<volatile unsigned*>(&s_rmax);
                     const int thr = rb > (int)kSpan ? rb - (int)kSpan : 1;  // bits of the threshold (> 0)
