@@ -347,23 +347,30 @@ __device__ __forceinline__ void grp_mask(Grp<SZ>& g, int e0, int lo, int hi)
 }
 
 // Segmented scans (rows of seg_len >= TILE elements: at most one row start per
-// tile).  The tile holding the first row start at or after tile t's first
-// element (INT_MAX if that start is at or past n), and the offset of the row
-// start inside tile t.  Evaluated once per job and once per row start, so the
-// hot tile loop carries one int and one compare.
+// tile).  A CTA's jobs of one phase visit its block of chunks 0, 1, 2, ... in
+// order, so the block start modulo seg_len advances by a constant per job: no
+// 64-bit division in the job loop (a division per job cost ~10 % of the kernel).
 template <int TILE>
-__device__ __forceinline__ int next_row_start_tile(int t, int64_t seg_len, int64_t n)
-{
-    const int64_t e = (int64_t)t * TILE;
-    const int64_t next = (e + seg_len - 1) / seg_len * seg_len;
-    return next < n ? (int)(next / TILE) : 0x7fffffff;
-}
-template <int TILE>
-__device__ __forceinline__ int row_start_offset(int t, int64_t seg_len)
-{
-    const int64_t e = (int64_t)t * TILE;
-    return (int)((e + seg_len - 1) / seg_len * seg_len - e);
-}
+struct SegCursor {
+    int64_t rem = 0;        // (first element of this CTA's block in the next job's chunk) mod seg_len
+    int tile = 0x7fffffff;  // tile of the next row start in the current job (INT_MAX: none before n)
+    int off = 0;            // its offset in that tile
+    __device__ __forceinline__ void init(int b, int bt, int64_t seg_len) { rem = ((int64_t)b * bt * TILE) % seg_len; }
+    __device__ __forceinline__ void set(int64_t next, int64_t n)
+    {
+        tile = next < n ? (int)(next / TILE) : 0x7fffffff;
+        off = (int)(next - (int64_t)tile * TILE);
+    }
+    // at the start of a job whose first tile is t0; dchunk = (chunk_tiles * TILE) mod seg_len
+    __device__ __forceinline__ void job(int t0, int64_t seg_len, int64_t dchunk, int64_t n)
+    {
+        set((int64_t)t0 * TILE + (rem == 0 ? 0 : seg_len - rem), n);
+        rem += dchunk;
+        if (rem >= seg_len) rem -= seg_len;
+    }
+    // after the row start in `tile` has been consumed
+    __device__ __forceinline__ void advance(int64_t seg_len, int64_t n) { set((int64_t)tile * TILE + off + seg_len, n); }
+};
 
 // One lane's 16 elements through a tile scan: load raw words, form the lane
 // total (int8: IDP.4A byte sums; others: the in-lane inclusive prefix v), then
@@ -876,6 +883,13 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
             m_out = (int)(ro < 0 ? 0 : (ro > m ? m : ro));
         };
 
+        SegCursor<TILE> seg_r, seg_s;  // SEG: row starts of the Phase-I / Phase-II jobs
+        int64_t seg_dc = 0;
+        if constexpr (SEG) {
+            seg_r.init(b, gm.bt, p.seg_len);
+            seg_s.init(b, gm.bt, p.seg_len);
+            seg_dc = ((int64_t)gm.chunk_tiles * TILE) % p.seg_len;
+        }
         for (int q = 0; q < njobs; ++q) {
             int c, t0, t1;
             bool is_scan;
@@ -884,15 +898,15 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
             if (!is_scan) {
                 // ---------------- Phase I: block reduction r[c][b] ----------------
                 Carry jsum = Carry(0);
-                int rs_tile = SEG ? next_row_start_tile<TILE>(t0, p.seg_len, gm.n) : 0x7fffffff;
+                if constexpr (SEG) seg_r.job(t0, p.seg_len, seg_dc, gm.n);
                 for (int t = t0; t < t1; ++t, rin.next()) {
                     mbar_wait_prof(&in_full[rin.s], rin.ph, prof0, &s_prof[1]);
                     const long long tr0 = prof ? clock64() : 0;
                     const uint8_t* slot = in_ring + rin.s * Cfg::kRingSlot;
-                    if (SEG && t == rs_tile) {
+                    if (SEG && t == seg_r.tile) {
                         // a row starts in this tile: drop the sums before it (cold path)
-                        const int ro = row_start_offset<TILE>(t, p.seg_len);
-                        rs_tile = next_row_start_tile<TILE>(t + 1, p.seg_len, gm.n);
+                        const int ro = seg_r.off;
+                        seg_r.advance(p.seg_len, gm.n);
                         int m = TILE, m_in = TILE, m_out = TILE;
                         if (t >= gm.full_tiles) ragged(t, m, m_in, m_out);
                         jsum = mc_split_sum<DT, GPW>(slot, gin_b + (int64_t)t * TILE * SZ, e0_base, m, m_in, ro);
@@ -929,7 +943,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 // ---------------- Phase II: scan with the block carry ----------------
                 mbar_wait_prof(&carry_ready[c % KC], (uint32_t)(c / KC) & 1u, prof0, &s_prof[0]);
                 Carry carry = s_carry[c % KC];
-                int rs_tile = SEG ? next_row_start_tile<TILE>(t0, p.seg_len, gm.n) : 0x7fffffff;
+                if constexpr (SEG) seg_s.job(t0, p.seg_len, seg_dc, gm.n);
                 for (int t = t0; t < t1; ++t, rin.next(), rout.next(), ++s_count) {
                     const int s = rin.s;
                     const int o = UNI ? s : rout.s;
@@ -940,9 +954,9 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     if (!full) ragged(t, m, m_in, m_out);
                     const uint8_t* slot = in_ring + s * Cfg::kRingSlot;
                     int ro = 0;
-                    if (SEG && t == rs_tile) {
-                        ro = row_start_offset<TILE>(t, p.seg_len);
-                        rs_tile = next_row_start_tile<TILE>(t + 1, p.seg_len, gm.n);
+                    if (SEG && t == seg_s.tile) {
+                        ro = seg_s.off;
+                        seg_s.advance(p.seg_len, gm.n);
                         if (ro == 0) carry = Carry(0);  // a row starts with this tile
                     }
                     if (SEG && ro > 0) {
