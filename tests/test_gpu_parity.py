@@ -356,7 +356,8 @@ def test_rows_short_and_few_long(cuda, oracle, inputs_mod, dt, exclusive):
     row); strided rows for the first two."""
     shapes = [(1000, 1), (777, 3), (513, 17), (300, 32), (257, 33), (129, 1000), (65, 2048),
               (33, 4095), (9, 4096), (3, (1 << 22) + 5),
-              (3, 1 << 19), (7, 12288 * 16), (2, 1 << 20), (150, 16384), (5, 300007), (40, 30011)]
+              (3, 1 << 19), (7, 12288 * 16), (2, 1 << 20), (150, 16384), (5, 300007), (40, 30011),
+              (74, 16384), (74, 24576), (74, 14200), (20, 65537)]
     for R, C in shapes:
         S = C + (16 if C < 8192 else 0)
         x = host_input(inputs_mod, dt, R * S, seed=R * 7 + C).reshape(R, S)
