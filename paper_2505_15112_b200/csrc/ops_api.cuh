@@ -463,8 +463,18 @@ int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t ro
     if (err != cudaSuccess) return SCAN_ERR_CUDA;
     const int per_sm = env_int("SCAN_TOPP_CTAS_PER_SM", occ) < occ ? env_int("SCAN_TOPP_CTAS_PER_SM", occ) : occ;
     const int64_t g = (int64_t)di.sms * per_sm < rows ? (int64_t)di.sms * per_sm : rows;
+    // row-ticket counter: the module's per-device array, one slot per launch (round robin)
+    static std::atomic<unsigned> launch_no{0};
+    static unsigned* tickets[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SCAN_ERR_CUDA;
+    if (tickets[dev] == nullptr &&
+        cudaGetSymbolAddress((void**)&tickets[dev], scan::topp::g_row_ticket) != cudaSuccess)
+        return SCAN_ERR_CUDA;
+    unsigned* ticket = tickets[dev] + launch_no.fetch_add(1, std::memory_order_relaxed) % scan::topp::kTicketSlots;
+    if (cudaMemsetAsync(ticket, 0, sizeof(unsigned), (cudaStream_t)stream) != cudaSuccess) return SCAN_ERR_CUDA;
     k_top_p<<<(unsigned)g, scan::topp::kThreads, smem, (cudaStream_t)stream>>>(probs, rows, cols, row_stride, p, u, token_out,
-                                                                    kept_out);
+                                                                    kept_out, ticket);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
 }

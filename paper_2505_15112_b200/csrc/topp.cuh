@@ -158,8 +158,16 @@ __device__ __forceinline__ float block_max(float v, float* s_red)
     return r;
 }
 
+// Row tickets: rows differ a lot in cost (superset size, level sizes, fallbacks),
+// so a CTA takes the next row when it is done instead of a fixed share -- with a
+// static grid-stride share the slowest CTA ran ~60 % longer than the median.
+// One counter per launch slot (the launcher zeroes it on the stream).
+constexpr int kTicketSlots = 64;
+__device__ unsigned int g_row_ticket[kTicketSlots];
+
 __global__ void __launch_bounds__(kThreads) k_top_p(const float* probs, int64_t rows, int64_t cols, int64_t stride,
-                                                    float p, const float* u, int64_t* token_out, int32_t* kept_out)
+                                                    float p, const float* u, int64_t* token_out, int32_t* kept_out,
+                                                    unsigned int* ticket)
 {
     extern __shared__ __align__(16) unsigned long long s_key[];  // kCap candidate keys, then kLevCap level keys
     unsigned long long* const s_lev = s_key + kCap;
@@ -179,7 +187,13 @@ __global__ void __launch_bounds__(kThreads) k_top_p(const float* probs, int64_t 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool vec = (cols % 4 == 0) && (stride % 4 == 0) && ((reinterpret_cast<uintptr_t>(probs) & 15) == 0);
 
-    for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    __shared__ int64_t s_row;
+    for (;;) {
+        if (tid == 0) s_row = (int64_t)atomicAdd(ticket, 1u);
+        __syncthreads();
+        const int64_t row = s_row;
+        __syncthreads();
+        if (row >= rows) break;
         const float* q = probs + row * stride;
         // 1-2 (fast path, one HBM read of the row): the row maximum and, in the same
         // pass, a candidate SUPERSET -- every q whose bits are within 53 * 2^21 of the
