@@ -47,6 +47,25 @@ __device__ __forceinline__ double key_val(unsigned long long k)
     return (double)__uint_as_float((uint32_t)(k >> 32) & 0x7fffffffu);
 }
 
+// Rank sort of keys[0, n) descending for n <= kLevCap / 2 (keys are distinct:
+// the index is part of the key): rank_i = #{ j : key_j > key_i }, computed by
+// every thread for its elements against all n (broadcast shared reads), the keys
+// placed at their ranks in tmp and copied back -- two barriers instead of the
+// bitonic network's log^2 n.
+__device__ void block_rank_sort_desc(unsigned long long* keys, int n, unsigned long long* tmp)
+{
+    const int tid = threadIdx.x;
+    for (int i = tid; i < n; i += kThreads) {
+        const unsigned long long ki = keys[i];
+        int r = 0;
+        for (int j = 0; j < n; ++j) r += keys[j] > ki ? 1 : 0;
+        tmp[r] = ki;
+    }
+    __syncthreads();
+    for (int i = tid; i < n; i += kThreads) keys[i] = tmp[i];
+    __syncthreads();
+}
+
 // Bitonic sort of keys[0, n) descending (padded with 0 keys to a power of two).
 __device__ void block_sort_desc(unsigned long long* keys, int n)
 {
@@ -402,7 +421,8 @@ __global__ void __launch_bounds__(kThreads) k_top_p(const float* probs, int64_t 
                     const int nL = block_extract_level(s_key, count, mb, L, s_lev, kLevCap, &s_cnt);
                     const double baseL = s_base;
                     const int nbefL = s_aux[0];
-                    block_sort_desc(s_lev, nL);
+                    if (nL <= kLevCap / 2) block_rank_sort_desc(s_lev, nL, s_lev + kLevCap / 2);
+                    else block_sort_desc(s_lev, nL);
                     const int jL = block_first_crossing<false>(s_lev, nL, baseL, (double)p, s_dred, &s_min, &s_c);
                     if (jL < nL) {  // always: cum(<= L) >= p
                         const int K = nbefL + jL + 1;
@@ -431,7 +451,8 @@ __global__ void __launch_bounds__(kThreads) k_top_p(const float* probs, int64_t 
                         if (ls != L) {
                             if (s_lcnt[ls] <= (unsigned)kLevCap) {
                                 nl = block_extract_level(s_key, count, mb, ls, s_lev, kLevCap, &s_cnt);
-                                block_sort_desc(s_lev, nl);
+                                if (nl <= kLevCap / 2) block_rank_sort_desc(s_lev, nl, s_lev + kLevCap / 2);
+                                else block_sort_desc(s_lev, nl);
                             } else {
                                 lev_ok = false;
                             }
