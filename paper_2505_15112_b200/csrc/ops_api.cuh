@@ -31,7 +31,9 @@ size_t split_ws_bytes(int64_t n)
     // 4096-element warp tile + the CTA totals (<= 4096 CTAs)
     const size_t a = (size_t)split_tiles4(n) * 8;
     const size_t b = (size_t)((split_wtiles(n) + 3) & ~(int64_t)3) * 8 + 4096 * 4;
-    return kSplitArrays + (a > b ? a : b) + 64;
+    const size_t c = (size_t)((n + scan::splitw::kSpWT - 1) / scan::splitw::kSpWT) * 8;  // single-pass compress
+    const size_t ab = a > b ? a : b;
+    return kSplitArrays + (ab > c ? ab : c) + 64;
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -126,6 +128,28 @@ int launch_split_warp(const SplitParams& sp, cudaStream_t s, const DevInfo& di)
     if (grid > 4096) grid = 4096;
     p.wpc = (p.nwt + grid - 1) / grid;
     grid = (p.nwt + p.wpc - 1) / p.wpc;
+    if (sp.compress && sp.idx_out == nullptr && getenv("SCAN_SPLIT_DIRECT") == nullptr &&
+        env_int("SCAN_COMPRESS_SP", 0)) {
+        // A/B only (DESIGN 5.6): single pass, decoupled look-back over 2048-element
+        // warp tiles -- 2.2x slower than the two passes (look-back distance ~ tiles in flight)
+        const int64_t nwt2 = (sp.n + kSpWT - 1) / kSpWT;
+        uint64_t* desc = reinterpret_cast<uint64_t*>(sp.counts);
+        unsigned* ticket = sp.hdr + 4;
+        if (cudaMemsetAsync(desc, 0, (size_t)nwt2 * 8, s) != cudaSuccess || cudaMemsetAsync(ticket, 0, 4, s) != cudaSuccess)
+            return SCAN_ERR_CUDA;
+        constexpr size_t smem = compress_sp_smem_bytes<ES>();
+        if (cudaFuncSetAttribute(k_compress_sp<ES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+            return SCAN_ERR_CUDA;
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_compress_sp<ES>, kSpThreads, smem) != cudaSuccess ||
+            occ < 1)
+            return SCAN_ERR_CUDA;
+        const int64_t wantc = (nwt2 + kSpThreads / 32 - 1) / (kSpThreads / 32);
+        const int64_t g = (int64_t)di.sms * occ < wantc ? (int64_t)di.sms * occ : wantc;
+        k_compress_sp<ES><<<(unsigned)g, kSpThreads, smem, s>>>(p, desc, ticket);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
+    }
     k_splitw_count<<<(unsigned)grid, kThreads, 0, s>>>(p);
     const int64_t want = ((int64_t)p.nwt + kWarps - 1) / kWarps;
     const int64_t g2 = (int64_t)di.sms * 4 < want ? (int64_t)di.sms * 4 : want;

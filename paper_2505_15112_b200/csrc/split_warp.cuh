@@ -461,5 +461,151 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_splitw_staged(const WParams p
     }
 }
 
+// ---- single-pass compress (decoupled look-back over warp tiles) ----------------
+// The two-pass compress reads the mask twice (5 B/element for 4 algorithmic:
+// ceiling 80 %, reached).  Here ONE pass: a warp claims the next 2048-element
+// warp tile by ticket (tiles start in order), loads its flags and payload into
+// registers, counts its trues, publishes the count (flag A) and looks back over
+// its predecessors' descriptors -- 32 at a time, summing aggregates back to the
+// nearest inclusive prefix (flag P) -- the decoupled look-back the paper cites
+// as the single-pass state of the art (P78-81); then it publishes its own
+// inclusive prefix, packs its trues into a shared-memory run aligned to the
+// destination (as k_splitw_staged) and writes it with 16-byte stores.  The
+// descriptor is one 64-bit word {flag:2 | value:62} (single-copy atomic: no
+// fences); the launcher zeroes the descriptors and the ticket on the stream.
+// Measured 2.2x SLOWER than the two passes (1.87 vs 0.86 ms at 2^30): with
+// ~3,500 warp tiles in flight the nearest published inclusive prefix is
+// typically thousands of tiles back, ~100 look-back windows of one L2 round
+// trip each -- the look-back distance grows with the concurrency B200 needs to
+// fill HBM.  Kept as an A/B (SCAN_COMPRESS_SP=1).
+constexpr int kSpWT = 2048;        // elements per warp tile
+constexpr int kSpSteps = kSpWT / 512;
+constexpr int kSpThreads = 256;
+constexpr uint64_t kSpA = 1ull << 62, kSpP = 2ull << 62, kSpVal = (1ull << 62) - 1;
+template <int ES>
+constexpr size_t compress_sp_smem_bytes() { return (size_t)(kSpThreads / 32) * (kSpWT + 32) * ES; }
+
+template <int ES>
+__global__ void __launch_bounds__(kSpThreads, 3) k_compress_sp(const WParams p, uint64_t* desc, unsigned* ticket)
+{
+    using P = typename std::conditional<ES == 2, uint16_t, uint8_t>::type;
+    constexpr int kMod = 16 / ES;  // elements per 16-byte vector
+    constexpr int kPW = ES;        // 16-byte payload vectors per lane per 512-element step
+    extern __shared__ __align__(16) uint8_t s_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    P* const z = reinterpret_cast<P*>(p.z);
+    P* const buf = reinterpret_cast<P*>(s_raw) + warp * (kSpWT + 32);
+    const int nwt = (int)((p.n + kSpWT - 1) / kSpWT);
+    for (;;) {
+        int wt = 0;
+        if (lane == 0) wt = (int)atomicAdd(ticket, 1u);
+        wt = __shfl_sync(0xffffffffu, wt, 0);
+        if (wt >= nwt) break;
+        const int64_t e0 = (int64_t)wt * kSpWT;
+        const bool full = e0 + kSpWT <= p.n;
+        uint32_t bits[kSpSteps];
+        uint4 pq[kSpSteps][kPW];
+        int tot = 0;
+        if (full) {
+            const uint4* fw = reinterpret_cast<const uint4*>(p.flags + e0);
+            const uint4* pw = reinterpret_cast<const uint4*>(reinterpret_cast<const P*>(p.x) + e0);
+            uint4 fq[kSpSteps];
+#pragma unroll
+            for (int k = 0; k < kSpSteps; ++k) {
+                fq[k] = __ldcs(fw + k * 32 + lane);
+#pragma unroll
+                for (int v = 0; v < kPW; ++v) pq[k][v] = __ldcs(pw + (k * 32 + lane) * kPW + v);
+            }
+            int c = 0;
+#pragma unroll
+            for (int k = 0; k < kSpSteps; ++k) {
+                bits[k] = nz_bits4(fq[k].x) | (nz_bits4(fq[k].y) << 4) | (nz_bits4(fq[k].z) << 8) |
+                          (nz_bits4(fq[k].w) << 12);
+                c += __popc(bits[k]);
+            }
+            tot = (int)__reduce_add_sync(0xffffffffu, (unsigned)c);
+        } else {
+            for (int64_t e = e0 + lane; e < e0 + 32 * ((p.n - e0 + 31) / 32); e += 32)
+                tot += __popc(__ballot_sync(0xffffffffu, e < p.n && p.flags[e] != 0));
+        }
+        // publish, look back, publish the inclusive prefix
+        uint64_t excl = 0;
+        if (wt == 0) {
+            if (lane == 0) ptx::st_relaxed_u64(desc, kSpP | (uint64_t)tot);
+        } else {
+            if (lane == 0) ptx::st_relaxed_u64(desc + wt, kSpA | (uint64_t)tot);
+            int64_t top = wt - 1;
+            uint32_t backoff = 16;
+            for (;;) {
+                const int64_t idx = top - lane;
+                const uint64_t d = idx >= 0 ? ptx::ld_relaxed_u64(desc + idx) : kSpP;  // before tile 0: prefix 0
+                if (__any_sync(0xffffffffu, (d >> 62) == 0)) {  // a predecessor has not published yet
+                    __nanosleep(backoff);
+                    backoff = backoff < 256 ? backoff * 2 : 256;
+                    continue;
+                }
+                const uint32_t pm = __ballot_sync(0xffffffffu, (d >> 62) == 2);
+                const int pl = pm ? __ffs(pm) - 1 : 32;  // the nearest inclusive prefix
+                uint64_t v = lane <= pl ? (d & kSpVal) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                excl += v;
+                if (pm) break;
+                top -= 32;
+            }
+            if (lane == 0) ptx::st_relaxed_u64(desc + wt, kSpP | (excl + (uint64_t)tot));
+        }
+        if (wt == nwt - 1 && lane == 0) {
+            reinterpret_cast<uint64_t*>(p.hdr)[1] = excl + (uint64_t)tot;
+            if (p.count_out) *p.count_out = (int64_t)(excl + (uint64_t)tot);
+        }
+        uint64_t tpos = excl;
+        if (full) {
+            const int shift = (int)(tpos % kMod);
+            int cT = 0;
+#pragma unroll
+            for (int k = 0; k < kSpSteps; ++k) {
+                const int c = __popc(bits[k]);
+                int incl = c;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += y;
+                }
+                uint32_t w[4 * kPW];
+#pragma unroll
+                for (int v = 0; v < kPW; ++v) {
+                    w[4 * v] = pq[k][v].x; w[4 * v + 1] = pq[k][v].y;
+                    w[4 * v + 2] = pq[k][v].z; w[4 * v + 3] = pq[k][v].w;
+                }
+                P* const dst = buf + shift + cT + (incl - c);
+                int kk = 0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    if ((bits[k] >> j) & 1u) {
+                        if constexpr (ES == 2) dst[kk] = (P)(w[j >> 1] >> (16 * (j & 1)));
+                        else dst[kk] = (P)(w[j >> 2] >> (8 * (j & 3)));
+                        ++kk;
+                    }
+                }
+                cT += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            __syncwarp();
+            write_run<P, kMod>(z + (tpos - (uint64_t)shift), buf, shift, cT, lane);
+            __syncwarp();
+        } else {
+            for (int64_t s0 = e0; s0 < p.n; s0 += 32) {
+                const int64_t e = s0 + lane;
+                const bool tr = e < p.n && p.flags[e] != 0;
+                const uint32_t bt = __ballot_sync(0xffffffffu, tr);
+                if (tr) z[tpos + __popc(bt & lt)] = reinterpret_cast<const P*>(p.x)[e];
+                tpos += __popc(bt);
+            }
+        }
+    }
+}
+
 }  // namespace splitw
 }  // namespace scan

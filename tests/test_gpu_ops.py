@@ -74,13 +74,16 @@ def test_split_unaligned(cuda, oracle, inputs_mod):
 
 
 @pytest.mark.parametrize("es", [1, 2])
-@pytest.mark.parametrize("direct", [False, True])
-def test_compress_no_indices(cuda, oracle, inputs_mod, monkeypatch, es, direct):
-    """compress without indices: the staged-run kernel (16-byte stores from a
-    per-warp run aligned to the destination) and the direct-store kernel, on the
-    recipe's mask and on all-true / all-false / sparse / alternating masks."""
-    if direct:
+@pytest.mark.parametrize("kernel", ["single_pass", "staged", "direct"])
+def test_compress_no_indices(cuda, oracle, inputs_mod, monkeypatch, es, kernel):
+    """compress without indices: the two-pass staged-run kernel (default; 16-byte
+    stores from a per-warp run aligned to the destination), the single-pass
+    look-back kernel (A/B) and the direct-store kernel, on the recipe's mask and
+    on all-true / all-false / sparse / alternating masks."""
+    if kernel == "direct":
         monkeypatch.setenv("SCAN_SPLIT_DIRECT", "1")
+    if kernel == "single_pass":
+        monkeypatch.setenv("SCAN_COMPRESS_SP", "1")
     for n in SIZES + [3 * 4096 + 17, 8192 * 5]:
         xd, xh = _payload(n, es, seed=n + 11 * es)
         rng = np.random.default_rng(n)
