@@ -235,14 +235,17 @@ int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, i
                 void* tmp_keys, int32_t* tmp_idx, cudaStream_t s, const DevInfo& di)
 {
     using namespace scan::radix;
+    // radix tiles (qualified: split::kTile / kThreads are also visible here)
+    constexpr int64_t kRT = scan::radix::kTile;
+    constexpr int kRThreads = scan::radix::kThreads;
     auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    const int64_t nt = (n + kTile - 1) / kTile;
+    const int64_t nt = (n + kRT - 1) / kRT;
     const int64_t nc = nt * kDigits;
     const size_t scan_ws = up(scan_rows_workspace_bytes(SCAN_I32_I32, kDigits, nt));
     uint32_t* counts = reinterpret_cast<uint32_t*>(w + scan_ws);
     uint32_t* offs = reinterpret_cast<uint32_t*>(w + scan_ws + up((size_t)nc * 4));
     uint32_t* dbase = reinterpret_cast<uint32_t*>(w + scan_ws + 2 * up((size_t)nc * 4));
-    const size_t smem = (size_t)kTile * (ES + 4);
+    const size_t smem = (size_t)kRT * (ES + 4);
     static std::once_flag once;
     static cudaError_t err = cudaSuccess;
     static int occ = 1;
@@ -258,7 +261,7 @@ int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, i
             err = cudaFuncSetAttribute(k_digit_scatter_tma<KT, ES, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)DigitTmaCfg<ES, false>::kSmem);
         if (err == cudaSuccess &&
-            (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_digit_scatter<KT, ES, true>, kThreads, smem) !=
+            (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_digit_scatter<KT, ES, true>, kRThreads, smem) !=
                  cudaSuccess ||
              occ < 1))
             occ = 1;
@@ -283,14 +286,14 @@ int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, i
         p.keys_out = (ps & 1) ? keys_out : tmp_keys;
         p.idx_out = (ps & 1) ? idx_out : tmp_idx;
         p.shift = 8 * ps;
-        k_digit_count<KT, ES><<<(unsigned)g_count, kThreads, 0, s>>>(p);
+        k_digit_count<KT, ES><<<(unsigned)g_count, kRThreads, 0, s>>>(p);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         // per digit, the exclusive scan of its tile counts: 256 rows of ntiles (P437 row scan)
         int st = scan_rows(counts, offs, kDigits, nt, nt, nt, SCAN_I32_I32, 1, w, scan_ws, s);
         if (st != SCAN_OK) return st;
         const bool tma = aligned16(src_k) && (src_i == nullptr || aligned16(src_i)) && getenv("SCAN_SORT_NO_TMA") == nullptr;
         if (tma) {
-            const int64_t g = (int64_t)di.sms < nt ? (int64_t)di.sms : nt;
+            const int64_t g = (int64_t)di.sms * RADIX_CTAS < nt ? (int64_t)di.sms * RADIX_CTAS : nt;
             if (src_i)
                 k_digit_scatter_tma<KT, ES, true><<<(unsigned)g, DigitTmaCfg<ES, true>::kThreadsT,
                                                     DigitTmaCfg<ES, true>::kSmem, s>>>(p);
@@ -298,9 +301,9 @@ int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, i
                 k_digit_scatter_tma<KT, ES, false><<<(unsigned)g, DigitTmaCfg<ES, false>::kThreadsT,
                                                      DigitTmaCfg<ES, false>::kSmem, s>>>(p);
         } else if (src_i) {
-            k_digit_scatter<KT, ES, true><<<(unsigned)g_scat, kThreads, smem, s>>>(p);
+            k_digit_scatter<KT, ES, true><<<(unsigned)g_scat, kRThreads, smem, s>>>(p);
         } else {
-            k_digit_scatter<KT, ES, false><<<(unsigned)g_scat, kThreads, smem, s>>>(p);
+            k_digit_scatter<KT, ES, false><<<(unsigned)g_scat, kRThreads, smem, s>>>(p);
         }
         g_launches.fetch_add(1, std::memory_order_relaxed);
         if (cudaGetLastError() != cudaSuccess) return SCAN_ERR_CUDA;

@@ -33,7 +33,16 @@ namespace radix {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kRounds = 16;                       // rounds of 32 elements per warp
+#ifndef RADIX_ROUNDS
+#define RADIX_ROUNDS 16
+#endif
+#ifndef RADIX_SMEM_KB
+#define RADIX_SMEM_KB 200
+#endif
+#ifndef RADIX_CTAS
+#define RADIX_CTAS 1
+#endif
+constexpr int kRounds = RADIX_ROUNDS;             // rounds of 32 elements per warp
 constexpr int kTile = kThreads * kRounds;         // 8192 elements per tile
 constexpr int kDigits = 256;
 
@@ -252,13 +261,14 @@ struct DigitTmaCfg {
     static constexpr int kIdxB = IDX_IN ? kTile * 4 : 0;
     static constexpr int kSlot = kKeyB + kIdxB;
     static constexpr int kStage = kTile * (ES + 4);
-    static constexpr int kNB = (200 * 1024 - kStage) / kSlot > 4 ? 4 : (200 * 1024 - kStage) / kSlot;
+    static constexpr int kBudget = RADIX_SMEM_KB * 1024;  // shared memory per CTA (2 CTAs per SM at <= 110 KB)
+    static constexpr int kNB = (kBudget - kStage) / kSlot > 4 ? 4 : (kBudget - kStage) / kSlot;
     static constexpr size_t kSmem = (size_t)kNB * kSlot + kStage;
     static constexpr int kThreadsT = kThreads + 32;
 };
 
 template <int KT, int ES, bool IDX_IN>
-__global__ void __launch_bounds__(kThreads + 32, 1) k_digit_scatter_tma(const DigitParams p)
+__global__ void __launch_bounds__(kThreads + 32, RADIX_CTAS) k_digit_scatter_tma(const DigitParams p)
 {
     using C = DigitTmaCfg<ES, IDX_IN>;
     constexpr int NB = C::kNB;
