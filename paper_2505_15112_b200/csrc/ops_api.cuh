@@ -107,7 +107,7 @@ int launch_split_tma(SplitParams& p, cudaStream_t s, const DevInfo& di)
 template <int ES>
 int launch_split_warp(const SplitParams& sp, cudaStream_t s, const DevInfo& di)
 {
-    using namespace scan::splitw;
+    using namespace scan::splitw;  // (kThreads qualified: split::kThreads is also visible)
     WParams p;
     memset(&p, 0, sizeof(p));
     p.x = sp.x;
@@ -150,7 +150,7 @@ int launch_split_warp(const SplitParams& sp, cudaStream_t s, const DevInfo& di)
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
     }
-    k_splitw_count<<<(unsigned)grid, kThreads, 0, s>>>(p);
+    k_splitw_count<<<(unsigned)grid, scan::splitw::kThreads, 0, s>>>(p);
     const int64_t want = ((int64_t)p.nwt + kWarps - 1) / kWarps;
     const int64_t g2 = (int64_t)di.sms * 4 < want ? (int64_t)di.sms * 4 : want;
     auto staged = [&](auto kern, size_t smem, int nt) -> int {
@@ -169,17 +169,17 @@ int launch_split_warp(const SplitParams& sp, cudaStream_t s, const DevInfo& di)
     int st = SCAN_OK;
     if (p.compress) {
         if (direct) {
-            if (p.idx_out) k_splitw_scatter<ES, true, true><<<(unsigned)g2, kThreads, 0, s>>>(p);
-            else k_splitw_scatter<ES, true, false><<<(unsigned)g2, kThreads, 0, s>>>(p);
+            if (p.idx_out) k_splitw_scatter<ES, true, true><<<(unsigned)g2, scan::splitw::kThreads, 0, s>>>(p);
+            else k_splitw_scatter<ES, true, false><<<(unsigned)g2, scan::splitw::kThreads, 0, s>>>(p);
         } else if (p.idx_out) {
             st = staged(k_splitw_staged<ES, true, true, 256>, staged_smem_bytes<ES, true, true, 256>(), 256);
         } else {
-            st = staged(k_splitw_staged<ES, true, false>, staged_smem_bytes<ES, true, false>(), kThreads);
+            st = staged(k_splitw_staged<ES, true, false>, staged_smem_bytes<ES, true, false>(), scan::splitw::kThreads);
         }
     } else {
         if (direct) {
-            if (p.idx_out) k_splitw_scatter<ES, false, true><<<(unsigned)g2, kThreads, 0, s>>>(p);
-            else k_splitw_scatter<ES, false, false><<<(unsigned)g2, kThreads, 0, s>>>(p);
+            if (p.idx_out) k_splitw_scatter<ES, false, true><<<(unsigned)g2, scan::splitw::kThreads, 0, s>>>(p);
+            else k_splitw_scatter<ES, false, false><<<(unsigned)g2, scan::splitw::kThreads, 0, s>>>(p);
         } else if (p.idx_out) {
             st = staged(k_splitw_staged<ES, false, true, 256>, staged_smem_bytes<ES, false, true, 256>(), 256);
         } else {
