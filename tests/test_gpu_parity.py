@@ -350,6 +350,24 @@ def test_shard_two_pass(cuda, oracle, inputs_mod, dt, exclusive):
 
 @pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
 @pytest.mark.parametrize("exclusive", [False, True])
+def test_rows_tiny_contiguous(cuda, oracle, inputs_mod, dt, exclusive):
+    """Contiguous rows of <= 32 columns take the shared-memory tile kernel
+    (k_rows_tile: 16-byte staged loads / stores, a thread per row); ragged last
+    tile (rows not a multiple of 256) and a ragged vector tail."""
+    for R, C in [(1, 1), (1000, 1), (777, 3), (513, 17), (300, 32), (256 * 3 + 5, 31)]:
+        x = host_input(inputs_mod, dt, R * C, seed=R * 13 + C).reshape(R, C)
+        got = cuda.rows(to_dev(x, dt), exclusive=exclusive)
+        torch.cuda.synchronize()
+        if dt in ("i32", "i8"):
+            assert np.array_equal(got.cpu().numpy(), oracle.rows(x, dt, exclusive=exclusive)), (R, C)
+        else:
+            y64, a64, _ = oracle.rows(x, dt, exclusive=exclusive)
+            bad, worst, at = oracle.check_f32(got.cpu().numpy(), y64, a64)
+            assert bad == 0, (R, C, worst, at)
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+@pytest.mark.parametrize("exclusive", [False, True])
 def test_rows_short_and_few_long(cuda, oracle, inputs_mod, dt, exclusive):
     """Row shapes of every row path: tiny rows (segmented warp scan, several
     rows per warp), short rows (a warp per row), few long rows (one MCScan per
