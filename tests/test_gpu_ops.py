@@ -215,7 +215,7 @@ def test_top_p_parity(cuda, oracle, inputs_mod, method):
         tok, kept = tok.cpu().numpy(), kept.cpu().numpy()
         agree = 0
         for r in range(R):
-            rt, rk = oracle.top_p_sample(P[r], p, float(u[r]))
+            rt, rk = oracle.top_p_sample(P[r], float(np.float32(p)), float(u[r]))  # p as the C ABI's fp32
             order = np.argsort(-P[r].astype(np.float64), kind="stable")
             C64 = np.cumsum(P[r][order].astype(np.float64))
             tol = 1e-6 * C64[-1] + 1e-6
@@ -232,7 +232,9 @@ def test_top_p_parity(cuda, oracle, inputs_mod, method):
 def test_top_p_select_edge_rows(cuda, oracle):
     """Sort-free top-p on hand-made rows: ties across the nucleus boundary
     (stable index order), a flat row that needs the sort fallback, zeros, a
-    single dominant token, a ragged column count."""
+    single dominant token, a ragged column count, a level of more than 2048 keys
+    (full candidate sort), many levels with ties in each (the draw's level ahead
+    of the nucleus level), a superset above 8192 candidates (re-read fallback)."""
     C = 50001
     rows = []
     r0 = np.zeros(C, np.float32); r0[[5, 17, 900, 40000]] = 0.25; rows.append(r0)     # 4-way tie
@@ -240,13 +242,32 @@ def test_top_p_select_edge_rows(cuda, oracle):
     r2 = np.zeros(C, np.float32); r2[123] = 1.0; rows.append(r2)                      # one token
     rng = np.random.default_rng(4)
     r3 = rng.random(C).astype(np.float32) ** 8; r3 /= r3.sum(); rows.append(r3)
+    r4 = np.zeros(C, np.float32); r4[rng.choice(C, 3000, replace=False)] = 1.0 / 3000; rows.append(r4)  # level > 2048
+    r5 = np.zeros(C, np.float32)                                                       # many levels, ties in each
+    for k in range(12):
+        r5[rng.choice(C, 40, replace=False)] += np.float32(2.0 ** -(k / 3.0))
+    r5 /= r5.sum(); rows.append(r5)
+    r6 = np.zeros(C, np.float32); r6[:10000] = 1e-4; rows.append(r6)                  # superset > 8192
     P = np.stack(rows)
-    u = np.array([0.1, 0.5, 0.9, 0.77], np.float32)
-    for p in (0.3, 0.6, 0.9):
+    u = np.array([0.1, 0.5, 0.9, 0.77, 0.3, 0.999, 0.6], np.float32)
+    for p in (0.05, 0.3, 0.6, 0.9, 0.999):
         tok, kept = cuda.top_p_sample(torch.from_numpy(P).cuda(), p, torch.from_numpy(u).cuda())
         for r in range(len(rows)):
-            rt, rk = oracle.top_p_sample(P[r], p, float(u[r]))
-            assert int(tok[r]) == rt and int(kept[r]) == rk, (p, r, int(tok[r]), rt, int(kept[r]), rk)
+            # the C ABI takes p as fp32: the oracle gets the same value
+            p32 = float(np.float32(p))
+            rt, rk = oracle.top_p_sample(P[r], p32, float(u[r]))
+            if r in (1, 6):
+                # more than 8192 candidates: the sort-path fallback (torch.sort + the fp32 row
+                # scan), exact only up to the scan tolerance -- check validity there
+                order = np.argsort(-P[r].astype(np.float64), kind="stable")
+                C64 = np.cumsum(P[r][order].astype(np.float64))
+                tol = 1e-6 * C64[-1] + 1e-6
+                K = int(kept[r])
+                assert K >= 1 and (K == C or C64[K - 1] >= p32 - tol) and (K == 1 or C64[K - 2] < p32 + tol)
+                rank = int(np.nonzero(order == int(tok[r]))[0][0])
+                assert rank < K and _valid_interval(C64, rank, float(u[r]) * C64[K - 1], tol), (p, r)
+            else:
+                assert int(tok[r]) == rt and int(kept[r]) == rk, (p, r, int(tok[r]), rt, int(kept[r]), rk)
 
 
 @pytest.mark.slow
