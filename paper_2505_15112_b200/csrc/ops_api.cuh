@@ -87,7 +87,7 @@ int launch_split_tma_c(SplitParams& p, cudaStream_t s, const DevInfo& di)
     if (err != cudaSuccess) return SCAN_ERR_CUDA;
     const int64_t want_count = ((int64_t)p.ntiles + kWarps - 1) / kWarps;
     const int64_t g_count = (int64_t)di.sms * 4 < want_count ? (int64_t)di.sms * 4 : want_count;
-    const int64_t g_scat = (int64_t)di.sms < p.ntiles ? (int64_t)di.sms : p.ntiles;
+    const int64_t g_scat = (int64_t)di.sms * C::kCtas < p.ntiles ? (int64_t)di.sms * C::kCtas : p.ntiles;
     k_split_count<SRC, ES, KT><<<(unsigned)g_count, kThreads, 0, s>>>(p);
     k_split_scatter_tma<SRC, ES, KT, IDX_IN, CMP><<<(unsigned)g_scat, C::kThreadsT, C::kSmem, s>>>(p);
     g_launches.fetch_add(2, std::memory_order_relaxed);

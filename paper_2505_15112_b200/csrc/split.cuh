@@ -450,6 +450,12 @@ __device__ __forceinline__ void write_run_packed(uint8_t* z, int32_t* idx, uint6
 // the ring depth instead of occupancy; 16 compute warps scan, stage and write.
 // One CTA per SM, tiles t = blockIdx.x + k * gridDim.x.  Requires 16-byte
 // aligned buffers; the ragged last tile is read straight from global memory.
+#ifndef SPLIT_SMEM_KB
+#define SPLIT_SMEM_KB 105
+#endif
+#ifndef SPLIT_CTAS
+#define SPLIT_CTAS 2
+#endif
 template <int SRC, int ES, bool IDX_IN>
 struct TmaCfg {
     static constexpr int kNC = kWarps;                        // compute warps (512 threads)
@@ -462,13 +468,16 @@ struct TmaCfg {
     // !IDX_IN and ES <= 2: one packed word per element, (payload << 16) | local index
     static constexpr bool kPack = !IDX_IN && ES <= 2;
     static constexpr int kStage = kPack ? (kTile + kSlack) * 4 : (kTile + kSlack) * (ES + 4);
-    static constexpr int kNB = (200 * 1024 - kStage) / kSlot > 4 ? 4 : (200 * 1024 - kStage) / kSlot;
+    // shared memory per CTA; the packed (!IDX_IN, ES <= 2) variants may run SPLIT_CTAS per SM
+    static constexpr int kCtas = (!IDX_IN && ES <= 2) ? SPLIT_CTAS : 1;
+    static constexpr int kBudget = (!IDX_IN && ES <= 2) ? SPLIT_SMEM_KB * 1024 : 200 * 1024;
+    static constexpr int kNB = (kBudget - kStage) / kSlot > 4 ? 4 : (kBudget - kStage) / kSlot;
     static constexpr size_t kSmem = (size_t)kNB * kSlot + kStage + 128;
 };
 
 // CMP: compress -- only the trues are staged and written.
 template <int SRC, int ES, int KT, bool IDX_IN, bool CMP = false>
-__global__ void __launch_bounds__(TmaCfg<SRC, ES, IDX_IN>::kThreadsT, 1) k_split_scatter_tma(const SplitParams p)
+__global__ void __launch_bounds__(TmaCfg<SRC, ES, IDX_IN>::kThreadsT, TmaCfg<SRC, ES, IDX_IN>::kCtas) k_split_scatter_tma(const SplitParams p)
 {
     using C = TmaCfg<SRC, ES, IDX_IN>;
     constexpr int NB = C::kNB;
