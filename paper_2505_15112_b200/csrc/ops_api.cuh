@@ -293,7 +293,8 @@ int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, i
         if (st != SCAN_OK) return st;
         const bool tma = aligned16(src_k) && (src_i == nullptr || aligned16(src_i)) && getenv("SCAN_SORT_NO_TMA") == nullptr;
         if (tma) {
-            const int64_t g = (int64_t)di.sms * RADIX_CTAS < nt ? (int64_t)di.sms * RADIX_CTAS : nt;
+            const int64_t ct = src_i ? DigitTmaCfg<ES, true>::kCtas : DigitTmaCfg<ES, false>::kCtas;
+            const int64_t g = (int64_t)di.sms * ct < nt ? (int64_t)di.sms * ct : nt;
             if (src_i)
                 k_digit_scatter_tma<KT, ES, true><<<(unsigned)g, DigitTmaCfg<ES, true>::kThreadsT,
                                                     DigitTmaCfg<ES, true>::kSmem, s>>>(p);

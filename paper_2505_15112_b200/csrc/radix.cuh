@@ -261,14 +261,17 @@ struct DigitTmaCfg {
     static constexpr int kIdxB = IDX_IN ? kTile * 4 : 0;
     static constexpr int kSlot = kKeyB + kIdxB;
     static constexpr int kStage = kTile * (ES + 4);
-    static constexpr int kBudget = RADIX_SMEM_KB * 1024;  // shared memory per CTA (2 CTAs per SM at <= 110 KB)
+    // shared memory per CTA: the first pass of 16-bit keys (no index input) may run RADIX_CTAS per SM
+    static constexpr bool kSmall = !IDX_IN && ES == 2;
+    static constexpr int kCtas = kSmall ? RADIX_CTAS : 1;
+    static constexpr int kBudget = kSmall ? RADIX_SMEM_KB * 1024 : 200 * 1024;
     static constexpr int kNB = (kBudget - kStage) / kSlot > 4 ? 4 : (kBudget - kStage) / kSlot;
     static constexpr size_t kSmem = (size_t)kNB * kSlot + kStage;
     static constexpr int kThreadsT = kThreads + 32;
 };
 
 template <int KT, int ES, bool IDX_IN>
-__global__ void __launch_bounds__(kThreads + 32, RADIX_CTAS) k_digit_scatter_tma(const DigitParams p)
+__global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas) k_digit_scatter_tma(const DigitParams p)
 {
     using C = DigitTmaCfg<ES, IDX_IN>;
     constexpr int NB = C::kNB;
