@@ -104,14 +104,20 @@ SCAN_API int scan_top_p_draw(const float* cdf, const int64_t* order, int64_t row
                              int64_t cdf_row_stride, int64_t order_row_stride, float p, const float* u,
                              int64_t* token_out, int32_t* kept_out, void* stream);
 
-/* Top-p sampling of `rows` rows WITHOUT a full sort (Sec. 5.5, R15): per row
- * the candidates {q >= tau} (tau lowered until their mass reaches p) are
- * sorted in shared memory by (probability descending, column ascending) --
- * the stable descending order -- scanned in fp64, and the nucleus / draw
- * taken as in scan_top_p_draw.  probs: row r at probs + r*row_stride, fp32,
+/* Top-p sampling of `rows` rows WITHOUT a full sort (Sec. 5.5, R15): per row,
+ * one read gathers the candidates near the row maximum, their exact masses per
+ * eighth-octave level locate the level where the nucleus ends, and only that
+ * level (and the draw's level) is ordered by (probability descending, column
+ * ascending) -- the stable descending order of the full sort; nucleus and draw
+ * as in scan_top_p_draw, with exact fp64 prefix sums (fallback: candidates
+ * {q >= tau}, tau lowered until their mass reaches p, all sorted).  p is used
+ * as given (fp32, widened exactly).  probs: row r at probs + r*row_stride, fp32,
  * non-negative; u [rows] uniform draws.  token_out [rows] int64 (-1: the row
  * needs more than 8192 candidates to reach p -- use the sort path,
- * scan_top_p_draw), kept_out NULL or [rows] int32 nucleus sizes. */
+ * scan_top_p_draw), kept_out NULL or [rows] int32 nucleus sizes.  Rows are
+ * claimed by ticket from a per-device counter slot (64, round robin): at most
+ * 64 calls in flight at once per device.  Errors: SCAN_ERR_ARG for cols == 0
+ * or >= 2^31 or null pointers (rows > 0), SCAN_ERR_CUDA for launch failures. */
 SCAN_API int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t row_stride, float p,
                                const float* u, int64_t* token_out, int32_t* kept_out, void* stream);
 

@@ -180,7 +180,9 @@ __device__ __forceinline__ float block_max(float v, float* s_red)
 // Row tickets: rows differ a lot in cost (superset size, level sizes, fallbacks),
 // so a CTA takes the next row when it is done instead of a fixed share -- with a
 // static grid-stride share the slowest CTA ran ~60 % longer than the median.
-// One counter per launch slot (the launcher zeroes it on the stream).
+// One counter per launch slot (the launcher zeroes it on the stream; slots are
+// reused round robin, so at most 64 top-p launches may be in flight at once per
+// device -- e.g. on 64 concurrent streams).
 constexpr int kTicketSlots = 64;
 __device__ unsigned int g_row_ticket[kTicketSlots];
 
