@@ -177,6 +177,78 @@ __device__ __forceinline__ float block_max(float v, float* s_red)
     return r;
 }
 
+// Warp-parallel level search (one warp): the first level l < lmax whose cumulative
+// mass (levels 0..l) reaches thr (STRICT: exceeds thr), the mass and count of the
+// levels before it; l = -1 if none.  Level masses are exact (fixed point), so the
+// sums are exact in any order.  Results in *out_l, *out_base, *out_nb (lane owning
+// the level, or lane 0 when none).
+template <bool STRICT>
+__device__ __forceinline__ void warp_first_level(const double* lvl, const unsigned* cnt, int lmax, double thr,
+                                                 int* out_l, double* out_base, int* out_nb)
+{
+    constexpr int kPL = (kLevels + 31) / 32;  // levels per lane, consecutive
+    const int lane = threadIdx.x & 31;
+    double v[kPL];
+    unsigned c[kPL];
+    double sv = 0.0;
+    unsigned sc = 0u;
+#pragma unroll
+    for (int k = 0; k < kPL; ++k) {
+        const int l = lane * kPL + k;
+        v[k] = l < lmax ? lvl[l] : 0.0;
+        c[k] = l < lmax ? cnt[l] : 0u;
+        sv += v[k];
+        sc += c[k];
+    }
+    double iv = sv;
+    unsigned ic = sc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double yv = __shfl_up_sync(0xffffffffu, iv, o);
+        const unsigned yc = __shfl_up_sync(0xffffffffu, ic, o);
+        if (lane >= o) {
+            iv += yv;
+            ic += yc;
+        }
+    }
+    double acc = __shfl_up_sync(0xffffffffu, iv, 1);
+    unsigned nacc = __shfl_up_sync(0xffffffffu, ic, 1);
+    if (lane == 0) {
+        acc = 0.0;
+        nacc = 0u;
+    }
+    unsigned first = 0xffffffffu;
+    double base = 0.0;
+    unsigned nb = 0u;
+#pragma unroll
+    for (int k = 0; k < kPL; ++k) {
+        const int l = lane * kPL + k;
+        if (l < lmax && first == 0xffffffffu) {
+            const double nx = acc + v[k];
+            if (STRICT ? nx > thr : nx >= thr) {
+                first = (unsigned)l;
+                base = acc;
+                nb = nacc;
+            } else {
+                acc = nx;
+                nacc += c[k];
+            }
+        }
+    }
+    const unsigned fl = __reduce_min_sync(0xffffffffu, first);
+    if (fl == 0xffffffffu) {
+        if (lane == 0) {
+            *out_l = -1;
+            *out_base = 0.0;
+            *out_nb = 0;
+        }
+    } else if (first == fl) {
+        *out_l = (int)fl;
+        *out_base = base;
+        *out_nb = (int)nb;
+    }
+}
+
 // Row tickets: rows differ a lot in cost (superset size, level sizes, fallbacks),
 // so a CTA takes the next row when it is done instead of a fixed share -- with a
 // static grid-stride share the slowest CTA ran ~60 % longer than the median.
@@ -186,7 +258,7 @@ __device__ __forceinline__ float block_max(float v, float* s_red)
 constexpr int kTicketSlots = 64;
 __device__ unsigned int g_row_ticket[kTicketSlots];
 
-__global__ void __launch_bounds__(kThreads) k_top_p(const float* probs, int64_t rows, int64_t cols, int64_t stride,
+__global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64_t rows, int64_t cols, int64_t stride,
                                                     float p, const float* u, int64_t* token_out, int32_t* kept_out,
                                                     unsigned int* ticket)
 {
@@ -394,32 +466,12 @@ __global__ void __launch_bounds__(kThreads) k_top_p(const float* probs, int64_t 
                     s_lcnt[l] = c;
                 }
                 __syncthreads();
-                if (tid == 0) {
-                    double cum = 0.0;
-                    int L = -1;
-                    for (int l = 0; l < kLevels; ++l) {
-                        cum += s_lvl[l];
-                        if (cum >= (double)p) {
-                            L = l;
-                            break;
-                        }
-                    }
-                    s_level = L;
-                }
+                // L = the first level whose cumulative mass reaches p; its base mass / count
+                if (warp == 0) warp_first_level<false>(s_lvl, s_lcnt, kLevels, (double)p, &s_level, &s_base, &s_aux[0]);
                 __syncthreads();
                 const int L = s_level;
                 if (L >= 0 && s_lcnt[L] <= (unsigned)kLevCap) {
                     // ---- level path: sort level L only (and the draw's level) ----
-                    if (tid == 0) {
-                        double base = 0.0;
-                        unsigned nb = 0;
-                        for (int l = 0; l < L; ++l) {
-                            base += s_lvl[l];
-                            nb += s_lcnt[l];
-                        }
-                        s_base = base;
-                        s_aux[0] = (int)nb;
-                    }
                     const int nL = block_extract_level(s_key, count, mb, L, s_lev, kLevCap, &s_cnt);
                     const double baseL = s_base;
                     const int nbefL = s_aux[0];
@@ -430,23 +482,11 @@ __global__ void __launch_bounds__(kThreads) k_top_p(const float* probs, int64_t 
                         const int K = nbefL + jL + 1;
                         const double CK = s_c;
                         const double t = (double)__ldg(u + row) * CK;
-                        if (tid == 0) {
-                            double cum = 0.0;
-                            int ls = L;
-                            unsigned nb = 0;
-                            for (int l = 0; l < L; ++l) {
-                                if (cum + s_lvl[l] > t) {
-                                    ls = l;
-                                    break;
-                                }
-                                cum += s_lvl[l];
-                                nb += s_lcnt[l];
-                            }
-                            s_base = cum;
-                            s_aux[1] = ls;
-                        }
+                        // the draw's level: the first level (< L) whose cumulative mass exceeds t
+                        __syncthreads();  // everyone has read s_base (baseL) above
+                        if (warp == 0) warp_first_level<true>(s_lvl, s_lcnt, L, t, &s_aux[1], &s_base, &s_aux[0]);
                         __syncthreads();
-                        const int ls = s_aux[1];
+                        const int ls = s_aux[1] < 0 ? L : s_aux[1];
                         const double base2 = s_base;
                         int nl = jL + 1;  // level L: only its nucleus part
                         bool lev_ok = true;
