@@ -96,19 +96,37 @@ __global__ void __launch_bounds__(kThreads) k_rows_tile(const SRParams p)
     const int64_t tiles = (p.rows + kThreads - 1) / kThreads;
     const In* in = reinterpret_cast<const In*>(p.in);
     Out* out = reinterpret_cast<Out*>(p.out);
+    // the next tile's 16-byte loads are issued into registers before this tile is
+    // scanned and stored (a thread holds at most kVPT vectors of a tile)
+    constexpr int kVPT = kTileMaxCols * kEs / 16;
+    uint4 pf[kVPT];
+    auto prefetch = [&](int64_t tt) {
+        const int64_t g0 = tt * tile_elems;
+        const int nv = tt < tiles ? (int)(min(tile_elems, total - g0) / kPerVec) : 0;
+#pragma unroll
+        for (int v = 0; v < kVPT; ++v) {
+            const int q = tid + v * kThreads;
+            pf[v] = q < nv ? __ldg(reinterpret_cast<const uint4*>(in + g0) + q) : make_uint4(0u, 0u, 0u, 0u);
+        }
+    };
+    prefetch(blockIdx.x);
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int64_t f0 = t * tile_elems;                   // multiple of 16 bytes (kThreads * cols * ES)
         const int ne = (int)min(tile_elems, total - f0);
-        // 1. stage: 16-byte loads, widened into padded shared memory
+        // 1. stage: the prefetched vectors, widened into padded shared memory
         const int nvec = ne / kPerVec;
-        for (int q = tid; q < nvec; q += kThreads) {
-            const uint4 w = __ldg(reinterpret_cast<const uint4*>(in + f0) + q);
-            const In* e = reinterpret_cast<const In*>(&w);
 #pragma unroll
-            for (int j = 0; j < kPerVec; ++j) s_v[pad32(q * kPerVec + j)] = widen(e[j]);
+        for (int v = 0; v < kVPT; ++v) {
+            const int q = tid + v * kThreads;
+            if (q < nvec) {
+                const In* e = reinterpret_cast<const In*>(&pf[v]);
+#pragma unroll
+                for (int j = 0; j < kPerVec; ++j) s_v[pad32(q * kPerVec + j)] = widen(e[j]);
+            }
         }
         for (int i = nvec * kPerVec + tid; i < ne; i += kThreads) s_v[pad32(i)] = widen(in[f0 + i]);
         __syncthreads();
+        prefetch(t + gridDim.x);
         // 2. thread tid scans row tid of the tile, in place
         if (tid * cols < ne) {
             Carry c = Carry(0);
