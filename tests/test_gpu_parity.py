@@ -109,6 +109,44 @@ def test_in_place(cuda, oracle, inputs_mod, dt):
     assert_parity(oracle, xd, oracle_1d(oracle, x, dt, False), dt)
 
 
+@pytest.mark.parametrize("n", [4096, 65536, 100000])
+def test_dependent_small_scans_pdl(cuda, oracle, inputs_mod, n):
+    """Small scans are launched with programmatic dependent launch: a scan that
+    reads the previous scan's output must still see all of it (the kernel waits
+    on griddepcontrol before its first global access).  Chains of dependent
+    scans, eagerly and replayed from a CUDA graph, against the oracle."""
+    x = host_input(inputs_mod, "i32", n, seed=n)
+    ref = x.copy()
+    for _ in range(3):
+        ref = oracle.inclusive(ref, "i32")
+    xd = to_dev(x, "i32")
+    a = torch.empty_like(xd)
+    b = torch.empty_like(xd)
+    c = torch.empty_like(xd)
+
+    def chain():
+        cuda.inclusive(xd, out=a)
+        cuda.inclusive(a, out=b)
+        cuda.inclusive(b, out=c)
+
+    chain()
+    torch.cuda.synchronize()
+    assert np.array_equal(c.cpu().numpy(), ref)
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        chain()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(4):
+                chain()
+    for _ in range(3):
+        c.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(c.cpu().numpy(), ref)
+
+
 def test_empty_and_errors(cuda):
     L = cuda.load()
     x = torch.empty(0, dtype=torch.int32, device="cuda")
