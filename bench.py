@@ -27,6 +27,8 @@ import subprocess
 import sys
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -196,22 +198,44 @@ def oracle_throughput(cfg: str, budget_s: float, chunk: int):
 
 
 def run_reference(args, rank):
-    """--impl reference: the CPU oracle as it stands, one bounded chunk per step."""
+    """--impl reference: the CPU oracle on the host cores (oracle_threaded.c:
+    the sequential oracle on contiguous chunks, one per core), each step one
+    scan of a bounded sample of the workload (the first 2^27 elements; C4:
+    the first 256 rows).  Rank 0 only."""
     if rank != 0:
         return 0
-    w = WORK[args.config]
-    chunk = w["n"] if args.config == "C1" else (1 << 24)
-    o = OracleStream(args.config, chunk)
+    import inputs
+    import oracle
+    cfg = args.config
+    w, c = WORK[cfg], inputs.CONFIGS[cfg]
+    cores = len(os.sched_getaffinity(0))
+    if cfg == "C4":
+        X = inputs.fill_host(c["kind"], c["seed"], 0, 256, w["n"])
+        out = np.empty(X.shape, np.float32)
+        nbytes = X.size * w["bpe"]
+        desc = f"first 256 rows of {w['rows']}"
+
+        def step():
+            oracle.scan_threaded_rows(X, w["dt"], threads=cores, out=out)
+    else:
+        cnt = min(w["n"], 1 << 27)
+        x = inputs.fill_host(c["kind"], c["seed"], 0, cnt)
+        out = np.empty(cnt, np.int32 if w["dt"] in ("i32", "i8") else np.float32)
+        nbytes = cnt * w["bpe"] * len(w["ops"])
+        desc = f"first {cnt} elements of {w['n']}"
+
+        def step():
+            for op in w["ops"]:
+                oracle.scan_threaded(x, w["dt"], exclusive=op == "exclusive", threads=cores, out=out)
     for _ in range(args.warmup):
-        o.step()
-    b = t = 0.0
+        step()
+    t0 = time.perf_counter()
     for _ in range(args.steps):
-        db, dt = o.step()
-        b += db
-        t += dt
-    value = b / t / 1e9
-    sample = f"{args.steps} steps x {chunk} {'rows-worth of elements' if args.config == 'C4' else 'elements'} " \
-             f"of the workload, single-thread C oracle (oracle/oracle_scan.c)"
+        step()
+    t = time.perf_counter() - t0
+    value = nbytes * args.steps / t / 1e9
+    sample = (f"{args.steps} steps, each one scan of the {desc} on {cores} host threads "
+              f"(oracle/oracle_threaded.c over oracle/oracle_scan.c)")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -219,8 +243,8 @@ def run_reference(args, rank):
         "scaling": "strong" if w["shard"] else "weak", "vs_baseline": None, "dtype": w["dtype"],
         "data": "synthetic (seeded counter-based generator, inputs/recipe.h)",
         "config": {"workload": w["name"]},
-        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                         "sample": sample},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -229,165 +253,289 @@ def run_reference(args, rank):
 
 
 # ----------------------------------------------------------------- ours
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baselines(cfg: str, seconds: float):
+    """cpu_baseline (rank 0, N = 1): the oracle on the GPU box's host cores.
+    All cores: oracle_threaded.c (chunk sums -> ordered carries -> chunk scans,
+    SURVEY 8(c5)) repeated over the workload's first 2^27 elements (C4: 256
+    rows); one core: the sequential oracle streamed over the leading chunks."""
+    import inputs
+    import oracle
+    w, c = WORK[cfg], inputs.CONFIGS[cfg]
+    cores = len(os.sched_getaffinity(0))
+    if cfg == "C4":
+        rows = 256
+        X = inputs.fill_host(c["kind"], c["seed"], 0, rows, w["n"])
+        x = X.reshape(-1)
+        desc = f"first {rows} rows of {w['rows']} (each row scanned independently, rows split over the threads)"
+    else:
+        cnt = min(w["n"], 1 << 27)
+        x = inputs.fill_host(c["kind"], c["seed"], 0, cnt)
+        desc = f"first {cnt} elements of {w['n']}"
+    out = np.empty(x.shape[0], np.int32 if w["dt"] in ("i32", "i8") else np.float32)
+    bytes_per = x.shape[0] * w["bpe"] * (2 if cfg == "C1" else 1)
+
+    def one():
+        if cfg == "C4":  # independent rows split over the threads
+            oracle.scan_threaded_rows(X, w["dt"], threads=cores, out=out.reshape(X.shape))
+        else:
+            for op in w["ops"]:
+                oracle.scan_threaded(x, w["dt"], exclusive=op == "exclusive", threads=cores, out=out)
+
+    one()
+    reps, t = 0, 0.0
+    while t < seconds / 2 or reps < 2:
+        t0 = time.perf_counter()
+        one()
+        t += time.perf_counter() - t0
+        reps += 1
+    v_all = bytes_per * reps / t / 1e9
+    v1, t1, sample1 = oracle_throughput(cfg, seconds / 2, 1 << 24)
+    return {"value": round(v_all, 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "variant": "oracle_threaded.c: chunk sums, ordered carries, chunk scans on every host core",
+            "cpu_model": cpu_model(),
+            "sample": f"{desc}, scanned {reps} times ({t:.1f} s) with {cores} threads",
+            "single_core": {"value": round(v1, 3), "unit": "GB/s", "cores": 1,
+                            "sample": f"{sample1}; {t1:.1f} s of single-thread oracle (oracle_scan.c)"}}
+
+
+class Run:
+    """One config on this rank: inputs in HBM, the step, its timing."""
+
+    def __init__(self, cfg, rank, world, dev):
+        import torch
+
+        from paper_2505_15112_b200 import dist as D
+        self.cfg, self.w = cfg, WORK[cfg]
+        self.rank, self.world, self.dev = rank, world, dev
+        w = self.w
+        self.sharded = w["shard"] and world > 1
+        self.total_elems = w["n"] * w["rows"]
+        if self.sharded:
+            lo, hi = D.shard_bounds(w["n"], world, rank)
+            self.x = make_input(cfg, lo, hi - lo, dev)
+            self.local_elems = hi - lo
+        else:
+            self.x = make_input(cfg, 0, w["rows"] if cfg == "C4" else w["n"], dev)
+            self.local_elems = self.total_elems
+        odt = torch.int32 if w["dt"] in ("i32", "i8") else torch.float32
+        self.out = torch.empty(self.x.shape, dtype=odt, device=dev)
+        self.out2 = torch.empty_like(self.out) if cfg == "C1" else None
+        self.scans_per_step = 2 if cfg == "C1" else 1
+        torch.cuda.synchronize()
+
+    def step(self, mark=None):
+        import paper_2505_15112_b200 as S
+        from paper_2505_15112_b200 import dist as D
+        cfg, w = self.cfg, self.w
+        if cfg == "C4":
+            S.rows(self.x, out=self.out)
+        elif cfg == "C1":
+            S.inclusive(self.x, out=self.out)
+            S.exclusive(self.x, out=self.out2)
+        elif self.sharded:
+            fn = D.sharded_exclusive if "exclusive" in w["ops"] else D.sharded_inclusive
+            fn(self.x, out=self.out, mark=mark)
+        else:
+            (S.exclusive if "exclusive" in w["ops"] else S.inclusive)(self.x, out=self.out)
+
+    def measure(self, steps, warmup, graph_opt, barrier, clocks=None):
+        """W warm-up steps, then K timed steps between barrier + synchronize;
+        CUDA events on the launching stream; max over ranks."""
+        import torch
+        import torch.distributed as dist
+
+        import paper_2505_15112_b200 as S
+        from paper_2505_15112_b200.dist import PHASES
+        stream = torch.cuda.current_stream()
+        for _ in range(warmup):
+            self.step()
+        torch.cuda.synchronize()
+        graph = None
+        if graph_opt or (graph_opt is None and self.cfg == "C1"):
+            # latency-bound sizes: the K steps captured back to back in one CUDA
+            # graph, so the timed region measures the GPU, not Python + ctypes
+            graph = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                self.step()
+            stream.wait_stream(side)
+            with torch.cuda.graph(graph):
+                for _ in range(steps):
+                    self.step()
+            graph.replay()
+            torch.cuda.synchronize()
+        ev_k, ev_ph = [], []
+
+        def ev():
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            return e
+
+        if clocks is not None:
+            clocks.start()
+            time.sleep(0.3)
+        barrier()
+        torch.cuda.synchronize()
+        l0 = S.launch_count()
+        t0 = ev()
+        if graph is not None:
+            graph.replay()
+        else:
+            for _ in range(steps):
+                if self.sharded:
+                    marks = []
+                    self.step(mark=lambda i: marks.append(ev()))
+                    ev_ph.append(marks)
+                else:
+                    a = ev()
+                    self.step()
+                    ev_k.append((a, ev()))
+        t1 = ev()
+        torch.cuda.synchronize()
+        barrier()
+        launches = S.launch_count() - l0
+        if graph is not None:  # replays launch the captured kernels without the host counter
+            launches = steps * self.scans_per_step
+        clk = clocks.stop() if clocks is not None else None
+        ms = t0.elapsed_time(t1)
+        phases = None
+        if graph is not None:
+            kernel_ms = ms / steps / self.scans_per_step  # per scan launch
+        elif self.sharded:
+            ph = [sum(m[i].elapsed_time(m[i + 1]) for m in ev_ph) / steps for i in range(len(PHASES))]
+            phases = dict(zip(PHASES, ph))
+            kernel_ms = phases["shard_scan"]
+        else:
+            kernel_ms = sum(a.elapsed_time(b) for a, b in ev_k) / steps
+        if self.world > 1:
+            vec = [ms, kernel_ms] + (list(phases.values()) if phases else [])
+            tt = torch.tensor(vec, dtype=torch.float64, device=self.dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            vals = tt.tolist()
+            ms, kernel_ms = vals[0], vals[1]
+            if phases:
+                phases = dict(zip(PHASES, vals[2:]))
+        ms_per_step = ms / steps
+        w = self.w
+        step_bytes = self.total_elems * w["bpe"] * self.scans_per_step
+        if not self.sharded and self.world > 1:
+            step_bytes *= self.world  # replicas: every rank scans the whole workload
+        value = step_bytes / (ms_per_step * 1e-3) / 1e9
+        local_bytes = self.local_elems * w["bpe"] * (self.scans_per_step if graph is None else 1)
+        peak, peak_src = peaks()
+        achieved = local_bytes / (kernel_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": recorded_traffic(self.cfg),
+                "peak_source": peak_src,
+                "note": ("achieved = algorithmic in+out bytes of the shard_scan launch (the dominant kernel of "
+                         "the RSS step) / its CUDA-event duration, max over ranks" if self.sharded else
+                         "achieved = algorithmic in+out bytes of the scan launch / its CUDA-event duration")}
+        self.graph = graph
+        return dict(ms=ms, ms_per_step=ms_per_step, kernel_ms=kernel_ms, phases=phases, launches=launches,
+                    value=value, step_bytes=step_bytes, local_bytes=local_bytes, roof=roof, clocks=clk,
+                    cuda_graph=graph is not None)
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     import paper_2505_15112_b200 as S
-    from paper_2505_15112_b200 import dist as D
 
     cfg = args.config
     w = WORK[cfg]
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     S.load()
-    sharded = w["shard"] and world > 1
-    total_elems = w["n"] * w["rows"]
-    if sharded:
-        lo, hi = D.shard_bounds(w["n"], world, rank)
-        x = make_input(cfg, lo, hi - lo, dev)
-        local_elems = hi - lo
-    elif cfg == "C4":
-        x = make_input(cfg, 0, w["rows"], dev)
-        local_elems = total_elems
-    else:
-        x = make_input(cfg, 0, w["n"], dev)
-        local_elems = total_elems
-    out_dtype = torch.int32 if w["dt"] in ("i32", "i8") else torch.float32
-    out = torch.empty(x.shape, dtype=out_dtype, device=dev)
-    out2 = torch.empty_like(out) if cfg == "C1" else None
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-
-    ev_k0, ev_k1 = [], []
-
-    def scan_call(xin, o, o2=None, timed=False):
-        if timed:
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-        if cfg == "C4":
-            S.rows(xin, out=o)
-        elif cfg == "C1":
-            S.inclusive(xin, out=o)
-            S.exclusive(xin, out=o2)
-        elif sharded:
-            (D.sharded_exclusive if "exclusive" in w["ops"] else D.sharded_inclusive)(xin, out=o)
-        else:
-            (S.exclusive if "exclusive" in w["ops"] else S.inclusive)(xin, out=o)
-        if timed:
-            b.record(stream)
-            ev_k0.append(a)
-            ev_k1.append(b)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    # ---- warm-up + timed device region
-    for _ in range(args.warmup):
-        scan_call(x, out, out2)
-    torch.cuda.synchronize()
-    graph = None
-    if args.graph or (args.graph is None and cfg == "C1"):
-        # Latency-bound sizes: capture one step in a CUDA graph and replay it,
-        # so the timed region measures the GPU, not Python + ctypes launch cost.
-        graph = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream()
-        side.wait_stream(stream)
-        with torch.cuda.stream(side):
-            scan_call(x, out, out2)
-        stream.wait_stream(side)
-        with torch.cuda.graph(graph):
-            for _ in range(args.steps):  # the K timed steps, back to back on the device
-                scan_call(x, out, out2)
-        graph.replay()
-        torch.cuda.synchronize()
-    clocks = ClockSampler(local_rank)
-    clocks.start()
-    time.sleep(0.3)
-    barrier()
-    torch.cuda.synchronize()
-    l0 = S.launch_count()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    if graph is not None:
-        graph.replay()
-    else:
-        for _ in range(args.steps):
-            scan_call(x, out, out2, timed=True)
-    t1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    launches = S.launch_count() - l0
-    if graph is not None:  # graph replays launch the captured kernels without the host counter
-        launches = args.steps * (2 if cfg == "C1" else 1)
-    clk = clocks.stop()
-    ms = t0.elapsed_time(t1)
-    if graph is not None:
-        kernel_ms = ms / args.steps / (2 if cfg == "C1" else 1)  # per scan launch
-    else:
-        kernel_ms = sum(a.elapsed_time(b) for a, b in zip(ev_k0, ev_k1)) / args.steps
-    if world > 1:
-        tt = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms, kernel_ms = tt.tolist()
-    ms_per_step = ms / args.steps
-    step_bytes = total_elems * w["bpe"] * (2 if cfg == "C1" else 1)
-    if not sharded and world > 1:
-        step_bytes *= world  # replicas: every rank scans the whole workload
-    value = step_bytes / (ms_per_step * 1e-3) / 1e9
-
-    # ---- roofline of the dominant kernel (the scan launch of each step)
-    peak, peak_src = peaks()
-    local_bytes = local_elems * w["bpe"] * (2 if cfg == "C1" and graph is None else 1)
-    achieved = local_bytes / (kernel_ms * 1e-3) / 1e9
-    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": recorded_traffic(cfg),
-            "peak_source": peak_src,
-            "note": "achieved = algorithmic in+out bytes of the scan launch / its CUDA-event duration"}
+    run = Run(cfg, rank, world, dev)
+    m = run.measure(args.steps, args.warmup, args.graph, barrier, clocks=ClockSampler(local_rank))
+    roof, value, ms_per_step = m["roof"], m["value"], m["ms_per_step"]
+    peak = roof["peak"]
 
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, x, out, out2, scan_call, dev, stream, world, barrier, local_elems, w,
-                      step_bytes)
-
-    # ---- CPU oracle baseline (rank 0, N = 1 only)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, t, sample = oracle_throughput(cfg, args.cpu_seconds, 1 << 24)
-        cpu = {"value": round(v, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
-               "sample": f"{sample}; {t:.1f} s of single-thread oracle time on the GPU box host"}
+        e2e = run_e2e(args, run, dev, world, barrier)
 
     # ---- same-run ceilings (SURVEY 8(d)), outside the timed region: the scan's
     # traffic as a pure stream (widen copy), a D2D memcpy of the same bytes, and
     # torch.cumsum (CUB) on the same input -- context for roofline.frac
     ceilings = None
     if world == 1 and cfg != "C1" and not args.no_ceilings:
-        ceilings = measure_ceilings(x, out, w, stream, local_bytes, kernel_ms)
+        ceilings = measure_ceilings(run.x, run.out, w, torch.cuda.current_stream(), m["local_bytes"],
+                                    m["kernel_ms"])
+    sharded, total_elems = run.sharded, run.total_elems
+    del run
+    torch.cuda.empty_cache()
+
+    # ---- the other BASELINE.json configs, device-resident, same timing rules
+    # (driver-side evidence for every config; the headline is the line's value)
+    others = None
+    if world == 1 and not args.no_other_configs:
+        others = {}
+        for c2 in sorted(WORK):
+            if c2 == cfg:
+                continue
+            r2 = Run(c2, rank, world, dev)
+            m2 = r2.measure(max(5, min(args.steps, 20)), 3, None, barrier)
+            others[c2] = {"workload": WORK[c2]["name"], "value": round(m2["value"], 1), "unit": "GB/s",
+                          "ms_per_step": round(m2["ms_per_step"], 5), "steps": max(5, min(args.steps, 20)),
+                          "pct_of_hbm_peak": round(100.0 * m2["value"] / peak, 2),
+                          "roofline": {k: m2["roof"][k] for k in ("achieved", "peak", "frac", "traffic")},
+                          "cuda_graph": m2["cuda_graph"], "gpu_launches": m2["launches"]}
+            del r2
+            torch.cuda.empty_cache()
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baselines(cfg, args.cpu_seconds)
 
     if rank == 0:
+        config = {
+            "workload": w["name"], "n_elements": total_elems, "bytes_per_step": m["step_bytes"],
+            "parallelism": (f"shard{world} (contiguous shards, NCCL all-gather of shard totals)"
+                            if sharded else (f"replicas x{world}" if world > 1 else "single GPU")),
+            "pct_of_hbm_peak": round(100.0 * value / (peak * world), 2),
+            "gelem_per_s": round(total_elems * (2 if cfg == "C1" else 1) * (world if not sharded and world > 1 else 1)
+                                 / (ms_per_step * 1e-3) / 1e9, 2),
+            "l2_flush": "not needed: inputs exceed the 126 MB L2" if m["local_bytes"] > (256 << 20)
+            else "hot L2 (latency-bound size)",
+            "cuda_graph": m["cuda_graph"],
+        }
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
             "higher_is_better": True, "scaling": "strong" if w["shard"] else "weak",
             "vs_baseline": None, "dtype": w["dtype"],
             "data": "synthetic (seeded counter-based generator, inputs/recipe.h; generated in HBM)",
-            "config": {
-                "workload": w["name"], "n_elements": total_elems, "bytes_per_step": step_bytes,
-                "parallelism": (f"shard{world} (contiguous shards, NCCL all-gather of shard totals)"
-                                if sharded else (f"replicas x{world}" if world > 1 else "single GPU")),
-                "pct_of_hbm_peak": round(100.0 * value / (peak * world), 2),
-                "gelem_per_s": round(total_elems * (2 if cfg == "C1" else 1) * (world if not sharded and world > 1 else 1)
-                                     / (ms_per_step * 1e-3) / 1e9, 2),
-                "l2_flush": "not needed: inputs exceed the 126 MB L2" if local_bytes > (256 << 20)
-                else "hot L2 (latency-bound size)",
-                "cuda_graph": graph is not None,
-            },
-            "roofline": roof, "ceilings": ceilings, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk,
+            "config": config, "roofline": roof,
         }
+        if m["phases"] is not None:
+            line["phases_ms"] = {k: round(v, 4) for k, v in m["phases"].items()}
+            line["phases_note"] = ("per step, mean over the timed steps, max over ranks: scan_shard_reduce "
+                                   "(pass 1), NCCL all-gather of the G totals, carry, scan_shard_scan (pass 2)")
+        line.update({"ceilings": ceilings, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": m["launches"],
+                     "clocks": m["clocks"]})
+        if others is not None:
+            line["other_configs"] = others
         print(json.dumps(line), flush=True)
     return 0
 
@@ -440,14 +588,17 @@ def measure_ceilings(x, out, w, stream, nbytes, scan_ms):
     return res
 
 
-def run_e2e(args, x, out, out2, scan_call, dev, stream, world, barrier, local_elems, w, step_bytes):
+def run_e2e(args, run, dev, world, barrier):
     """Same metric through the public API with HOST buffers: every step moves
-    the input from pinned host memory and the result back.  1-D scans use the
-    library's pipelined host path (scan_host: chunked H2D / scan / D2H on
-    three streams); rows and C1 copy whole arrays around the device call."""
+    the input from pinned host memory and the result back.  1-D scans at N = 1
+    use the library's pipelined host path (scan_host: chunked H2D / scan / D2H
+    on three streams); rows, C1 and sharded steps copy whole arrays around the
+    device step."""
     import torch
 
     import paper_2505_15112_b200 as S
+    x, out, out2, w = run.x, run.out, run.out2, run.w
+    stream = torch.cuda.current_stream()
     h_in = torch.empty(x.shape, dtype=x.dtype, pin_memory=True)
     h_in.copy_(x)
     h_out = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
@@ -461,7 +612,7 @@ def run_e2e(args, x, out, out2, scan_call, dev, stream, world, barrier, local_el
             S.host_scan(h_in, h_out, exclusive=exclusive, chunk=args.e2e_chunk)
             return
         x.copy_(h_in, non_blocking=True)
-        scan_call(x, out, out2)
+        run.step()
         h_out.copy_(out, non_blocking=True)
         if h_out2 is not None:
             h_out2.copy_(out2, non_blocking=True)
@@ -487,8 +638,30 @@ def run_e2e(args, x, out, out2, scan_call, dev, stream, world, barrier, local_el
     d2h = out.numel() * out.element_size() * (2 if out2 is not None else 1)
     path = ("pinned host -> scan_host (C ABI: chunked H2D | scan | D2H on 3 streams) -> pinned host"
             if pipelined else "pinned host -> cudaMemcpyAsync -> scan (C ABI) -> cudaMemcpyAsync -> pinned host")
+    step_bytes = run.total_elems * w["bpe"] * run.scans_per_step * (world if not run.sharded and world > 1 else 1)
     return {"value": round(step_bytes / (ms / steps * 1e-3) / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps, "path": path}
+
+
+def relaunch(args) -> int:
+    """`--gpus N` (N > 1) without a torch.distributed environment: start N ranks
+    (one process per GPU, NCCL) with torch.distributed.run on 127.0.0.1 and
+    return its exit code.  Fails loudly if this node has fewer than N GPUs."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        log(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, this node has {have}")
+        return 1
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    log("bench.py: launching " + " ".join(cmd[2:]))
+    return subprocess.call(cmd)
 
 
 def main():
@@ -504,6 +677,8 @@ def main():
     ap.add_argument("--e2e-chunk", type=int, default=1 << 26, help="elements per host-streaming chunk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-other-configs", action="store_true",
+                    help="skip timing the other BASELINE.json configs after the main line")
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
                     help="replay each step from a CUDA graph (default: on for C1 only)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
@@ -512,11 +687,17 @@ def main():
         log("warmup raised to 3 (contract minimum)")
         args.warmup = 3
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world_env = os.environ.get("WORLD_SIZE")
+    world = int(world_env or "1")
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank)
+    if world_env is None and args.gpus > 1:
+        return relaunch(args)
+    if world != args.gpus:
+        log(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+        return 2
     if world > 1:
         import torch
         import torch.distributed as dist

@@ -49,8 +49,18 @@
  *     bytes, initialised ONCE with scan_workspace_init() before first use,
  *     then reusable by any number of calls issued in stream order.  Two
  *     calls that may run concurrently must not share a workspace.
- *   - Thread safety: calls are reentrant; the library's only state is a
- *     per-device cache of device attributes.
+ *   - Operators (scan_ops.h: split / compress, radix sort) keep scratch in
+ *     the workspace where look-back descriptors live.  The library records
+ *     (host side) which workspaces an operator dirtied, and the next
+ *     scan_inclusive / scan_exclusive / scan_rows given that workspace zeroes
+ *     that range first (one cudaMemsetAsync on its stream).  A CUDA graph that
+ *     captured a scan does not see this record: do not share a graph's
+ *     workspace with operator calls outside the graph.
+ *   - Thread safety: calls are reentrant.  The library's state: per-device
+ *     caches of device attributes and kernel attributes (set once per
+ *     device), the dirty-workspace record above, and, for scan_host only,
+ *     two copy streams per device created on first use and kept for the
+ *     life of the process.
  */
 #ifndef PAPER_2505_15112_B200_SCAN_H
 #define PAPER_2505_15112_B200_SCAN_H
@@ -62,7 +72,7 @@
 extern "C" {
 #endif
 
-#define SCAN_ABI_VERSION 1
+#define SCAN_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define SCAN_API __attribute__((visibility("default")))

@@ -115,11 +115,15 @@ SCAN_API int scan_top_p_draw(const float* cdf, const int64_t* order, int64_t row
  * non-negative; u [rows] uniform draws.  token_out [rows] int64 (-1: the row
  * needs more than 8192 candidates to reach p -- use the sort path,
  * scan_top_p_draw), kept_out NULL or [rows] int32 nucleus sizes.  Rows are
- * claimed by ticket from a per-device counter slot (64, round robin): at most
- * 64 calls in flight at once per device.  Errors: SCAN_ERR_ARG for cols == 0
- * or >= 2^31 or null pointers (rows > 0), SCAN_ERR_CUDA for launch failures. */
+ * claimed by ticket from a counter in the header of `ws` (a workspace
+ * initialised with scan_workspace_init, at least scan_workspace_bytes(dtype, 0)
+ * bytes; calls that may run concurrently need distinct workspaces).  Errors:
+ * SCAN_ERR_ARG for cols == 0 or >= 2^31 or null pointers (rows > 0),
+ * SCAN_ERR_WORKSPACE for a NULL / misaligned / too small ws, SCAN_ERR_CUDA for
+ * launch failures. */
 SCAN_API int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t row_stride, float p,
-                               const float* u, int64_t* token_out, int32_t* kept_out, void* stream);
+                               const float* u, int64_t* token_out, int32_t* kept_out, void* ws,
+                               size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -53,7 +53,7 @@ def build() -> str:
 def lib():
     global _lib
     if _lib is None:
-        srcs = [os.path.join(_HERE, f) for f in ("oracle_scan.c", "oracle_ops.c")]
+        srcs = [os.path.join(_HERE, f) for f in ("oracle_scan.c", "oracle_ops.c", "oracle_threaded.c")]
         if (not os.path.exists(_LIB_PATH)
                 or os.path.getmtime(_LIB_PATH) < max(os.path.getmtime(f) for f in srcs)):
             build()
@@ -79,6 +79,11 @@ def lib():
         L.oracle_check_f32.restype = I64
         L.oracle_rows_f32.argtypes = [P, I64, I64, I64, I64, I, P, P, P]
         L.oracle_rows_i32.argtypes = [P, I64, I64, I64, I64, I, P]
+        # oracle_threaded.c: the all-core CPU baseline (bench.py cpu_baseline only)
+        L.oracle_scan_threaded.argtypes = [P, I64, I, I, I, P]
+        L.oracle_scan_threaded.restype = I
+        L.oracle_rows_threaded.argtypes = [P, I64, I64, I, I, I, P]
+        L.oracle_rows_threaded.restype = I
         # oracle_ops.c: scan applications (Sec. 5, App. B.3)
         L.oracle_split.argtypes = [P, P, I64, I, I, P, P]
         L.oracle_split.restype = I64
@@ -164,6 +169,38 @@ def exclusive(x, dt: str, carry_in=None):
     if dt in (I32, I8):
         return IntScan(dt, 0 if carry_in is None else carry_in)(x, True)
     return FloatScan(dt, 0.0 if carry_in is None else carry_in)(x, True)
+
+
+_DT_CODE = {I32: 0, F32: 1, F16: 2, I8: 3}
+
+
+def scan_threaded(x, dt: str, exclusive: bool = False, threads: int = 1, out=None):
+    """All-core BASELINE (oracle_threaded.c): the scan split over
+    `threads` host threads (chunk sums, ordered carries, chunk scans).  int32
+    output for integer types (bit-identical to inclusive()/exclusive()), fp32
+    for float types (fp64 carries; a timing baseline, never a checker)."""
+    x = _as_input(x, dt)
+    n = x.shape[0]
+    if out is None:
+        out = np.empty(n, np.int32 if dt in (I32, I8) else np.float32)
+    rc = lib().oracle_scan_threaded(_ptr(x), n, _DT_CODE[dt], int(exclusive), int(threads), _ptr(out))
+    if rc != 0:
+        raise RuntimeError("oracle_scan_threaded failed")
+    return out
+
+
+def scan_threaded_rows(X, dt: str, exclusive: bool = False, threads: int = 1, out=None):
+    """All-core BASELINE for row batches: rows split over `threads` host
+    threads, each row scanned by the sequential oracle (identical results)."""
+    X = np.ascontiguousarray(X)
+    R, C = X.shape
+    x = _as_input(X.reshape(-1), dt)
+    if out is None:
+        out = np.empty((R, C), np.int32 if dt in (I32, I8) else np.float32)
+    rc = lib().oracle_rows_threaded(_ptr(x), R, C, _DT_CODE[dt], int(exclusive), int(threads), _ptr(out))
+    if rc != 0:
+        raise RuntimeError("oracle_rows_threaded failed")
+    return out
 
 
 def total(x, dt: str):

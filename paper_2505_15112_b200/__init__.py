@@ -106,7 +106,7 @@ def load() -> ctypes.CDLL:
         L.scan_weighted_sample.restype = I
         L.scan_top_p_draw.argtypes = [P, P, I64, I64, I64, I64, ctypes.c_float, P, P, P, P]
         L.scan_top_p_draw.restype = I
-        L.scan_top_p_sample.argtypes = [P, I64, I64, I64, ctypes.c_float, P, P, P, P]
+        L.scan_top_p_sample.argtypes = [P, I64, I64, I64, ctypes.c_float, P, P, P, P, SZ, P]
         L.scan_top_p_sample.restype = I
         _lib = L
     return _lib
@@ -130,12 +130,17 @@ def _ptr(t):
 class Workspace:
     """A caller-owned, initialised workspace (device uint8 buffer).
 
-    One per (device, stream) is cached by ``workspace()``; it grows on demand
-    and is re-initialised (scan_workspace_init) whenever it is reallocated."""
+    One per (device, stream, kind) is cached by ``workspace()``; it grows on
+    demand and is re-initialised (scan_workspace_init) whenever it is
+    reallocated.  The buffer is allocated on the stream that uses it, so the
+    caching allocator never hands its memory to another stream while kernels
+    queued there may still touch it."""
 
     def __init__(self, nbytes: int, device, stream=None):
         nbytes = max(int(nbytes), 1 << 16)
-        self.buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+        s = stream if stream is not None else torch.cuda.current_stream(device)
+        with torch.cuda.stream(s):
+            self.buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
         off = (-self.buf.data_ptr()) % 256
         self.nbytes = nbytes
         self.ptr = self.buf.data_ptr() + off
@@ -146,11 +151,15 @@ class Workspace:
 _ws_cache: dict = {}
 
 
-def workspace(nbytes: int, device=None, stream=None) -> Workspace:
+def workspace(nbytes: int, device=None, stream=None, kind: str = "scan") -> Workspace:
+    """The cached workspace of (device, stream, kind).  Scans and the scan
+    operators (kind="ops": split / compress / sort / top-p) keep separate
+    buffers, so operator scratch never sits where a scan's look-back
+    descriptors go (the C library also clears such scratch, see scan.h)."""
     dev = torch.device(device) if device is not None else torch.device("cuda",
                                                                        torch.cuda.current_device())
     s = stream if stream is not None else torch.cuda.current_stream(dev)
-    key = (dev.index, s.cuda_stream)
+    key = (dev.index, s.cuda_stream, kind)
     ws = _ws_cache.get(key)
     if ws is None or ws.nbytes < nbytes:
         ws = Workspace(max(nbytes, 2 * (ws.nbytes if ws else 0)), dev, s)
@@ -204,15 +213,19 @@ def rows(X: torch.Tensor, exclusive: bool = False, out=None, stream=None) -> tor
     if X.dim() != 2 or (X.shape[1] > 1 and X.stride(1) != 1):
         raise ScanError("rows() expects a 2-D tensor with unit column stride")
     R, C = X.shape
+    if R > 1 and X.stride(0) < C:  # expanded / overlapping rows: scan a dense copy
+        X = X.contiguous()
     if out is None:
         out = torch.empty((R, C), dtype=odt, device=X.device)
     elif out.dtype != odt or tuple(out.shape) != (R, C) or (C > 1 and out.stride(1) != 1):
         raise ScanError(f"out must be a {odt} tensor of shape {(R, C)} with unit column stride")
+    elif R > 1 and out.stride(0) < C:
+        raise ScanError("out rows overlap (row stride < cols)")
     in_stride = X.stride(0) if R > 1 else C
     out_stride = out.stride(0) if R > 1 else C
     L = load()
     ws = workspace(L.scan_rows_workspace_bytes(dt, R, C), X.device, stream)
-    _check(L.scan_rows(_ptr(X), _ptr(out), R, C, max(in_stride, C), max(out_stride, C), dt,
+    _check(L.scan_rows(_ptr(X), _ptr(out), R, C, in_stride, out_stride, dt,
                        int(bool(exclusive)), ctypes.c_void_p(ws.ptr), ws.nbytes,
                        _stream_ptr(stream)), "scan_rows")
     return out
@@ -355,7 +368,7 @@ def split(x: torch.Tensor, flags: torch.Tensor, compress: bool = False, with_idx
         if with_idx else None
     cnt = torch.empty(1, dtype=torch.int64, device=x.device)
     L = load()
-    ws = workspace(L.scan_split_workspace_bytes(n), x.device, stream)
+    ws = workspace(L.scan_split_workspace_bytes(n), x.device, stream, kind="ops")
     _check(L.scan_split(_ptr(x), _ptr(flags), _ptr(z), _ptr(idx), n, x.element_size(), int(bool(compress)),
                         _ptr(cnt), ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)), "scan_split")
     return z, idx, cnt
@@ -384,7 +397,7 @@ def radix_sort(keys: torch.Tensor, descending: bool = False, out=None, idx_out=N
     idx = torch.empty(n, dtype=torch.int32, device=keys.device) if idx_out is None else idx_out
     L = load()
     kt = SCAN_KEY[keys.dtype]
-    ws = workspace(L.scan_radix_sort_workspace_bytes(n, kt), keys.device, stream)
+    ws = workspace(L.scan_radix_sort_workspace_bytes(n, kt), keys.device, stream, kind="ops")
     _check(L.scan_radix_sort(_ptr(keys), _ptr(kout), _ptr(idx), n, kt, int(bool(descending)),
                              ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)), "scan_radix_sort")
     return kout, idx
@@ -427,8 +440,10 @@ def top_p_sample(probs: torch.Tensor, p: float, u: torch.Tensor, stream=None, me
     tok = torch.empty(R, dtype=torch.int64, device=probs.device)
     kept = torch.empty(R, dtype=torch.int32, device=probs.device)
     if method == "select":
+        ws = workspace(0, probs.device, stream, kind="ops")
         _check(load().scan_top_p_sample(_ptr(probs), R, C, probs.stride(0) if R > 1 else C, float(p), _ptr(u),
-                                        _ptr(tok), _ptr(kept), _stream_ptr(stream)), "scan_top_p_sample")
+                                        _ptr(tok), _ptr(kept), ctypes.c_void_p(ws.ptr), ws.nbytes,
+                                        _stream_ptr(stream)), "scan_top_p_sample")
         miss = torch.nonzero(tok < 0).flatten()
         if miss.numel() == 0:
             return tok, kept

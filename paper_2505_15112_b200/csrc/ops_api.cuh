@@ -49,10 +49,10 @@ int launch_split_t(SplitParams& p, cudaStream_t s, const DevInfo& di)
 {
     using namespace scan::split;
     const size_t smem = (size_t)kTile * (ES + 4);
-    static std::once_flag once;
+    static DevOnce once;
     static cudaError_t err = cudaSuccess;
     static int occ = 1;
-    std::call_once(once, [smem] {
+    dev_call_once(once, [smem] {
         err = cudaFuncSetAttribute(k_split_scatter<SRC, ES, KT, IDX_IN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem);
         if (err == cudaSuccess &&
@@ -78,9 +78,9 @@ int launch_split_tma_c(SplitParams& p, cudaStream_t s, const DevInfo& di)
 {
     using namespace scan::split;
     using C = TmaCfg<SRC, ES, IDX_IN>;
-    static std::once_flag once;
+    static DevOnce once;
     static cudaError_t err = cudaSuccess;
-    std::call_once(once, [] {
+    dev_call_once(once, [] {
         err = cudaFuncSetAttribute(k_split_scatter_tma<SRC, ES, KT, IDX_IN, CMP>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
     });
@@ -246,10 +246,10 @@ int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, i
     uint32_t* offs = reinterpret_cast<uint32_t*>(w + scan_ws + up((size_t)nc * 4));
     uint32_t* dbase = reinterpret_cast<uint32_t*>(w + scan_ws + 2 * up((size_t)nc * 4));
     const size_t smem = (size_t)kRT * (ES + 4);
-    static std::once_flag once;
+    static DevOnce once;
     static cudaError_t err = cudaSuccess;
     static int occ = 1;
-    std::call_once(once, [smem] {
+    dev_call_once(once, [smem] {
         err = cudaFuncSetAttribute(k_digit_scatter<KT, ES, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (err == cudaSuccess)
             err = cudaFuncSetAttribute(k_digit_scatter<KT, ES, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -351,6 +351,7 @@ int scan_split(const void* x, const int8_t* flags, void* z, int32_t* idx_out, in
     p.compress = compress != 0;
     p.aligned = aligned16(x) && aligned16(z) && aligned16(flags) && (idx_out == nullptr || aligned16(idx_out));
     using namespace scan::split;
+    ws_mark_dirty(ws, split_ws_bytes(n));  // tile counts / offsets sit where look-back descriptors go
     switch (elem_bytes) {
     case 1: return launch_split<SRC_FLAGS, 1, 0>(p, s, di);
     case 2: return launch_split<SRC_FLAGS, 2, 0>(p, s, di);
@@ -378,8 +379,21 @@ size_t scan_radix_sort_workspace_bytes(int64_t n, int key_type)
     return (a > b ? a : b) + up((size_t)n * es) + up((size_t)n * 4);
 }
 
+static int radix_sort_impl(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, int key_type,
+                           int descending, void* ws, size_t ws_bytes, void* stream);
+
 int scan_radix_sort(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, int key_type, int descending,
                     void* ws, size_t ws_bytes, void* stream)
+{
+    const int st = radix_sort_impl(keys, keys_out, idx_out, n, key_type, descending, ws, ws_bytes, stream);
+    // counts, offsets and the key / index temporaries sit where look-back
+    // descriptors go: the next scan call given this workspace clears them
+    if (st == SCAN_OK && n > 0) ws_mark_dirty(ws, scan_radix_sort_workspace_bytes(n, key_type));
+    return st;
+}
+
+static int radix_sort_impl(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, int key_type,
+                           int descending, void* ws, size_t ws_bytes, void* stream)
 {
     if (n < 0 || n >= ((int64_t)1 << 31) || key_type < SCAN_KEY_U16 || key_type > SCAN_KEY_F32) return SCAN_ERR_ARG;
     const size_t need = scan_radix_sort_workspace_bytes(n, key_type);
@@ -468,21 +482,22 @@ int scan_top_p_draw(const float* cdf, const int64_t* order, int64_t rows, int64_
 }
 
 int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t row_stride, float p, const float* u,
-                      int64_t* token_out, int32_t* kept_out, void* stream)
+                      int64_t* token_out, int32_t* kept_out, void* ws, size_t ws_bytes, void* stream)
 {
     if (rows < 0 || cols < 0 || row_stride < cols) return SCAN_ERR_ARG;
     if (rows == 0) return SCAN_OK;
     if (cols == 0 || cols >= ((int64_t)1 << 31) || probs == nullptr || u == nullptr || token_out == nullptr)
         return SCAN_ERR_ARG;
+    if (ws == nullptr || ((uintptr_t)ws & 255u) != 0 || ws_bytes < kWsDescOffset) return SCAN_ERR_WORKSPACE;
     DevInfo di;
     int st = dev_info(di);
     if (st != SCAN_OK) return st;
     using namespace scan::topp;
     const size_t smem = kSmemBytes;
-    static std::once_flag once;
+    static DevOnce once;
     static cudaError_t err = cudaSuccess;
     static int occ = 1;
-    std::call_once(once, [smem] {
+    dev_call_once(once, [smem] {
         err = cudaFuncSetAttribute(k_top_p, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (err == cudaSuccess &&
             (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_top_p, scan::topp::kThreads, smem) != cudaSuccess || occ < 1))
@@ -491,15 +506,8 @@ int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t ro
     if (err != cudaSuccess) return SCAN_ERR_CUDA;
     const int per_sm = env_int("SCAN_TOPP_CTAS_PER_SM", occ) < occ ? env_int("SCAN_TOPP_CTAS_PER_SM", occ) : occ;
     const int64_t g = (int64_t)di.sms * per_sm < rows ? (int64_t)di.sms * per_sm : rows;
-    // row-ticket counter: the module's per-device array, one slot per launch (round robin)
-    static std::atomic<unsigned> launch_no{0};
-    static unsigned* tickets[64] = {};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SCAN_ERR_CUDA;
-    if (tickets[dev] == nullptr &&
-        cudaGetSymbolAddress((void**)&tickets[dev], scan::topp::g_row_ticket) != cudaSuccess)
-        return SCAN_ERR_CUDA;
-    unsigned* ticket = tickets[dev] + launch_no.fetch_add(1, std::memory_order_relaxed) % scan::topp::kTicketSlots;
+    // row-ticket counter: in the caller's workspace header
+    unsigned* ticket = reinterpret_cast<unsigned*>((uint8_t*)ws + scan::topp::kTicketWsOffset);
     if (cudaMemsetAsync(ticket, 0, sizeof(unsigned), (cudaStream_t)stream) != cudaSuccess) return SCAN_ERR_CUDA;
     k_top_p<<<(unsigned)g, scan::topp::kThreads, smem, (cudaStream_t)stream>>>(probs, rows, cols, row_stride, p, u, token_out,
                                                                     kept_out, ticket);

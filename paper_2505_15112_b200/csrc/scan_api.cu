@@ -58,6 +58,68 @@ int dev_info(DevInfo& out)
     return out.ok ? SCAN_OK : SCAN_ERR_DEVICE;
 }
 
+// Per-device one-time setup (cudaFuncSetAttribute is a per-device setting: a
+// process that drives several GPUs must set it on each of them).
+struct DevOnce {
+    std::mutex mu;
+    bool done[64] = {};
+};
+
+template <class F>
+void dev_call_once(DevOnce& o, F&& f)
+{
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+    std::lock_guard<std::mutex> g(o.mu);
+    if (!o.done[dev]) {
+        f();
+        o.done[dev] = true;
+    }
+}
+
+// Workspaces whose descriptor region holds operator scratch (split counts,
+// radix temporaries) that a later look-back scan could misread as tagged
+// descriptors.  The operators register the range they dirtied; the next scan
+// entry point that receives the workspace zeroes it (stream-ordered) before
+// launching -- a zero slot never carries a live epoch (epochs are >= 1).
+struct DirtyWs {
+    uintptr_t base;
+    size_t bytes;
+};
+std::mutex g_dirty_mu;
+DirtyWs g_dirty[256];
+int g_ndirty = 0;
+
+void ws_mark_dirty(void* ws, size_t bytes)
+{
+    std::lock_guard<std::mutex> g(g_dirty_mu);
+    const uintptr_t b = (uintptr_t)ws;
+    for (int i = 0; i < g_ndirty; ++i)
+        if (g_dirty[i].base == b) {
+            if (bytes > g_dirty[i].bytes) g_dirty[i].bytes = bytes;
+            return;
+        }
+    if (g_ndirty == 256) {  // full: forget the oldest (its owner can re-init it)
+        memmove(&g_dirty[0], &g_dirty[1], sizeof(DirtyWs) * 255);
+        g_ndirty = 255;
+    }
+    g_dirty[g_ndirty++] = {b, bytes};
+}
+
+// Bytes of `ws` (from its start) to zero before a scan, 0 if clean.
+size_t ws_take_dirty(const void* ws, size_t ws_bytes)
+{
+    std::lock_guard<std::mutex> g(g_dirty_mu);
+    const uintptr_t b = (uintptr_t)ws;
+    for (int i = 0; i < g_ndirty; ++i)
+        if (g_dirty[i].base == b) {
+            const size_t d = g_dirty[i].bytes < ws_bytes ? g_dirty[i].bytes : ws_bytes;
+            g_dirty[i] = g_dirty[--g_ndirty];
+            return d;
+        }
+    return 0;
+}
+
 bool valid_dt(int dt) { return dt >= 0 && dt <= 3; }
 size_t in_size(int dt) { return dt == SCAN_I32_I32 || dt == SCAN_F32_F32 ? 4 : dt == SCAN_F16_F32 ? 2 : 1; }
 size_t out_size(int) { return 4; }
@@ -90,10 +152,10 @@ struct Variant {
 
     static int occupancy()
     {
-        static std::once_flag once;
+        static DevOnce once;
         static int occ = 0;
         static cudaError_t err = cudaSuccess;
-        std::call_once(once, [] {
+        dev_call_once(once, [] {
             auto kern = k_scan_tiles<DT, TH, RW, ST, OS, MB>;
             err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
             if (err == cudaSuccess)
@@ -105,10 +167,10 @@ struct Variant {
     // Small 1-D n (2..16 tiles): one cluster, one tile per CTA, DSMEM carries.
     static int launch_cluster(ScanParams p, cudaStream_t s)
     {
-        static std::once_flag once;
+        static DevOnce once;
         static cudaError_t err = cudaSuccess;
         auto kern = k_scan_tiles<DT, TH, RW, ST, OS, MB>;
-        std::call_once(once, [&] {
+        dev_call_once(once, [&] {
             err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
             if (err == cudaSuccess)
                 err = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -183,9 +245,9 @@ struct WsVariant {
 
     static int ready()
     {
-        static std::once_flag once;
+        static DevOnce once;
         static cudaError_t err = cudaSuccess;
-        std::call_once(once, [] {
+        dev_call_once(once, [] {
             err = cudaFuncSetAttribute(k_scan_ws<DT, NC, NL, RW, NBI, NBO>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
         });
@@ -266,9 +328,9 @@ struct Mc16Variant {
         // segmented: rows of >= one tile (at most one row start per tile); the
         // in-place ring would let a split tile's first pass overwrite its inputs
         if (segmented && (sp.seg_len < kTile || Cfg::kUni)) return SCAN_ERR_ARG;
-        static std::once_flag once;
+        static DevOnce once;
         static cudaError_t err = cudaSuccess;
-        std::call_once(once, [] {
+        dev_call_once(once, [] {
             err = cudaFuncSetAttribute(k_mcscan16<DT, NC, GPW, NBI, NBO, SEG>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
         });
@@ -406,9 +468,9 @@ struct RowVariant {
     static int launch(const ScanParams& sp, cudaStream_t s, const DevInfo& di)
     {
         using In = typename Traits<DT>::In;
-        static std::once_flag once;
+        static DevOnce once;
         static cudaError_t err = cudaSuccess;
-        std::call_once(once, [] {
+        dev_call_once(once, [] {
             err = cudaFuncSetAttribute(k_rowscan16<DT, NC, GPW, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)Cfg::kSmem);
         });
@@ -454,9 +516,9 @@ template <int ES>
 int launch_rows_tc(const ScanParams& sp, cudaStream_t s, const DevInfo& di)
 {
     using Cfg = scan::tc::TcCfg<ES>;
-    static std::once_flag once;
+    static DevOnce once;
     static cudaError_t err = cudaSuccess;
-    std::call_once(once, [] {
+    dev_call_once(once, [] {
         err = cudaFuncSetAttribute(scan::tc::k_rowscan_tc<ES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)Cfg::kSmem);
     });
@@ -653,6 +715,16 @@ int check_ws(int dt, void* ws, size_t ws_bytes, int64_t tiles_needed)
     return SCAN_OK;
 }
 
+// Zero the operator scratch a previous split / sort left in `ws` (see DirtyWs).
+int ws_clean(void* ws, size_t ws_bytes, cudaStream_t s)
+{
+    if (ws == nullptr) return SCAN_OK;
+    const size_t d = ws_take_dirty(ws, ws_bytes);
+    if (d > kWsDescOffset && cudaMemsetAsync((uint8_t*)ws + kWsDescOffset, 0, d - kWsDescOffset, s) != cudaSuccess)
+        return SCAN_ERR_CUDA;
+    return SCAN_OK;
+}
+
 int scan_1d(const void* in, void* out, int64_t n, int dt, const void* carry_in, void* ws,
             size_t ws_bytes, void* stream, int exclusive)
 {
@@ -681,6 +753,7 @@ int scan_1d(const void* in, void* out, int64_t n, int dt, const void* carry_in, 
     p.exclusive = exclusive;
     p.tma_in = ((uintptr_t)in & 15u) == 0;
     p.tma_out = ((uintptr_t)out & 15u) == 0;
+    if ((st = ws_clean(ws, ws_bytes, (cudaStream_t)stream)) != SCAN_OK) return st;
     return launch_any(dt, p, (cudaStream_t)stream, di);
 }
 
@@ -783,6 +856,7 @@ int scan_rows(const void* in, void* out, int64_t rows, int64_t cols, int64_t in_
     p.exclusive = exclusive ? 1 : 0;
     p.tma_in = ((uintptr_t)in & 15u) == 0 && ((in_row_stride * (int64_t)in_size(dtype)) & 15) == 0;
     p.tma_out = ((uintptr_t)out & 15u) == 0 && ((out_row_stride * 4) & 15) == 0;
+    if ((st = ws_clean(ws, ws_bytes, (cudaStream_t)stream)) != SCAN_OK) return st;
     return launch_any(dtype, p, (cudaStream_t)stream, di);
 }
 

@@ -252,11 +252,10 @@ __device__ __forceinline__ void warp_first_level(const double* lvl, const unsign
 // Row tickets: rows differ a lot in cost (superset size, level sizes, fallbacks),
 // so a CTA takes the next row when it is done instead of a fixed share -- with a
 // static grid-stride share the slowest CTA ran ~60 % longer than the median.
-// One counter per launch slot (the launcher zeroes it on the stream; slots are
-// reused round robin, so at most 64 top-p launches may be in flight at once per
-// device -- e.g. on 64 concurrent streams).
-constexpr int kTicketSlots = 64;
-__device__ unsigned int g_row_ticket[kTicketSlots];
+// The counter lives in the caller's workspace header (the launcher zeroes it on
+// the stream before the launch), so concurrent or graph-captured calls with
+// distinct workspaces never share it.
+constexpr size_t kTicketWsOffset = 192;  // inside the 256-byte workspace header pad
 
 __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64_t rows, int64_t cols, int64_t stride,
                                                     float p, const float* u, int64_t* token_out, int32_t* kept_out,

@@ -35,28 +35,52 @@ def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
     return lo, hi
 
 
+PHASES = ("shard_reduce", "all_gather", "carry", "shard_scan")
+
+
 def rss_scan(x_local, exclusive: bool, rank: int, world: int,
              local_total: Callable, all_gather: Callable, carry_of: Callable,
-             local_scan: Callable):
+             local_scan: Callable, mark: Callable | None = None):
     """Device-level Reduce-Scan-Scan over `world` ranks (host orchestration only).
 
     local_total(x)             -> 1-element tensor (int64 / float64)
     all_gather(t)              -> tensor of `world` totals in rank order
     carry_of(totals, rank)     -> 1-element carry tensor
     local_scan(x, exclusive, carry) -> the rank's output shard
+    mark(i)                    -> optional, called at the phase boundaries
+                                  i = 0..4 (before PHASES[0] ... after PHASES[3]),
+                                  e.g. to record CUDA events for per-phase timing
     """
+    mark = mark or (lambda i: None)
+    mark(0)
     t = local_total(x_local)
+    mark(1)
     totals = all_gather(t)
+    mark(2)
     carry = carry_of(totals, rank)
-    return local_scan(x_local, exclusive, carry), totals, carry
+    mark(3)
+    y = local_scan(x_local, exclusive, carry)
+    mark(4)
+    return y, totals, carry
 
 
-def _nccl_all_gather(group):
+def _all_gather(group):
+    """All-gather of one total per rank, in rank order.  NCCL: one
+    all_gather_into_tensor of G x 8 bytes over NVLink / NVSwitch, stream-ordered
+    with the scan kernels.  Host backends (gloo: the multi-process tests on one
+    GPU, where ranks must not exchange through device memory): the 8-byte
+    totals travel through host memory."""
+    backend = dist.get_backend(group)
+
     def gather(t):
         world = dist.get_world_size(group)
-        out = torch.empty(world * t.numel(), dtype=t.dtype, device=t.device)
-        dist.all_gather_into_tensor(out, t, group=group)
-        return out
+        if backend == "nccl":
+            out = torch.empty(world * t.numel(), dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(out, t, group=group)
+            return out
+        parts = [torch.empty(t.shape, dtype=t.dtype) for _ in range(world)]
+        dist.all_gather(parts, t.cpu(), group=group)
+        return torch.cat(parts).to(t.device)
     return gather
 
 
@@ -75,7 +99,7 @@ def _shard_ws(x_local: torch.Tensor):
     return ws
 
 
-def _sharded(x_local: torch.Tensor, exclusive: bool, group=None, out=None, ws=None):
+def _sharded(x_local: torch.Tensor, exclusive: bool, group=None, out=None, ws=None, mark=None):
     from . import carry_from_totals, shard_reduce, shard_scan
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
@@ -86,18 +110,19 @@ def _sharded(x_local: torch.Tensor, exclusive: bool, group=None, out=None, ws=No
 
     y, _, _ = rss_scan(x_local, exclusive, rank, world,
                        local_total=lambda x: shard_reduce(x, ws=ws),
-                       all_gather=_nccl_all_gather(group),
+                       all_gather=_all_gather(group),
                        carry_of=lambda totals, r: carry_from_totals(totals, r, x_local.dtype),
-                       local_scan=local_scan)
+                       local_scan=local_scan, mark=mark)
     return y
 
 
-def sharded_inclusive(x_local: torch.Tensor, group=None, out=None, ws=None) -> torch.Tensor:
+def sharded_inclusive(x_local: torch.Tensor, group=None, out=None, ws=None, mark=None) -> torch.Tensor:
     """Inclusive scan of the array whose rank-r contiguous shard is x_local
-    (`ws`: a reusable paper_2505_15112_b200.shard_workspace for this shard)."""
-    return _sharded(x_local, False, group, out, ws)
+    (`ws`: a reusable paper_2505_15112_b200.shard_workspace for this shard;
+    `mark`: see rss_scan)."""
+    return _sharded(x_local, False, group, out, ws, mark)
 
 
-def sharded_exclusive(x_local: torch.Tensor, group=None, out=None, ws=None) -> torch.Tensor:
+def sharded_exclusive(x_local: torch.Tensor, group=None, out=None, ws=None, mark=None) -> torch.Tensor:
     """Exclusive scan of the array whose rank-r contiguous shard is x_local."""
-    return _sharded(x_local, True, group, out, ws)
+    return _sharded(x_local, True, group, out, ws, mark)

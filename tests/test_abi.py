@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol():
     L = S.load()
     for name in declared_symbols():
         assert hasattr(L, name), name
-    assert L.scan_abi_version() == 1
+    assert L.scan_abi_version() == 2
     # host-only calls work without a GPU
     assert L.scan_workspace_bytes(0, 0) >= 256
     assert L.scan_workspace_bytes(7, 10) == 0

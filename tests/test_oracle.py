@@ -370,3 +370,95 @@ def test_rows_equal_per_row(oracle, inputs_mod):
     Yi = oracle.rows(Xi, "i32")
     for r in range(4):
         assert np.array_equal(Yi[r], oracle.inclusive(Xi[r], "i32"))
+
+
+def test_total_f16_pins(oracle, inputs_mod):
+    """oracle_total_f16 (the checker of the GPU's fp16 scan_total / shard sums).
+    C2-type data: every value is k*2^-24, so the exact total is an int64 count
+    of 2^-24 units (< 2^53: exact in fp64) -- the fp64 sequential sum must equal
+    it bit for bit.  N(0,1) fp16 data: within n*2^-53*sum|x| of math.fsum over
+    numpy's own binary16 decode.  Specials: inf / NaN propagate."""
+    n = 1 << 20
+    h = inputs_mod.fill_host(inputs_mod.F16_U01, 1, 0, n)
+    k = np.round(h.view(np.float16).astype(np.float64) * 2.0 ** 24).astype(np.int64)
+    assert oracle.total(h, "f16") == float(int(k.sum())) * 2.0 ** -24
+    g = inputs_mod.fill_host(inputs_mod.F16_NORMAL, 9, 0, 300001)
+    v = g.view(np.float16).astype(np.float64)
+    exact = math.fsum(v.tolist())
+    assert abs(oracle.total(g, "f16") - exact) <= len(v) * 2.0 ** -53 * float(np.abs(v).sum())
+    assert oracle.total(g, "f16") != oracle.total(g[:-1], "f16") or v[-1] == 0.0  # last element counted
+    sp = np.array([0x3C00, 0x7C00, 0x3C00], np.uint16)              # 1, +inf, 1
+    assert oracle.total(sp, "f16") == math.inf
+    sp = np.array([0x7C00, 0xFC00], np.uint16)                      # +inf + -inf
+    assert math.isnan(oracle.total(sp, "f16"))
+    assert oracle.total(np.array([0x8001, 0x0001], np.uint16), "f16") == 0.0   # -/+ smallest subnormal
+    assert oracle.total(np.array([0x0001] * 3, np.uint16), "f16") == 3 * 2.0 ** -24
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32"])
+def test_rows_exclusive_pins(oracle, inputs_mod, dt):
+    """The exclusive branch of oracle_rows_* (P461 per row, P437): brute force
+    with Python integers (exact, mod 2^32 for int32; small-integer floats are
+    exact in fp64), e[r][0] = 0 as +0.0, and e[r] = (0, inclusive shifted)."""
+    R, C = 7, 333
+    rng = np.random.default_rng(11)
+    if dt == "i32":
+        X = rng.integers(-(1 << 31), 1 << 31, (R, C), dtype=np.int64).astype(np.int32)
+        E = oracle.rows(X, "i32", exclusive=True)
+        I = oracle.rows(X, "i32")
+        for r in range(R):
+            acc = 0
+            for i in range(C):
+                assert E[r, i] == wrap32(acc), (r, i)
+                acc += int(X[r, i])
+            assert np.array_equal(E[r], np.concatenate([[0], I[r, :-1]]))
+    else:
+        X = rng.integers(-1000, 1001, (R, C)).astype(np.float32)
+        e64, ea, e32 = oracle.rows(X, "f32", exclusive=True)
+        i64, ia, i32 = oracle.rows(X, "f32")
+        for r in range(R):
+            acc = 0
+            for i in range(C):
+                assert e64[r, i] == float(acc) and e32[r, i] == np.float32(acc), (r, i)
+                acc += int(X[r, i])
+            assert not np.signbit(e64[r, 0])
+            assert np.array_equal(e64[r, 1:], i64[r, :-1])
+            # tolerance weight: A_i = sum_{j<=i}|x_j| for exclusive too (R7)
+            assert np.array_equal(ea[r], np.cumsum(np.abs(X[r].astype(np.int64))).astype(np.float64))
+        P = inputs_mod.fill_host(inputs_mod.F32_SOFTMAX, 3, 0, 3, 4096)
+        p64, _, _ = oracle.rows(P, "f32", exclusive=True)
+        q64, _, _ = oracle.rows(P, "f32")
+        assert np.all(p64[:, 0] == 0.0) and np.array_equal(p64[:, 1:], q64[:, :-1])
+
+
+@pytest.mark.parametrize("dt", ["i32", "i8", "f32", "f16"])
+def test_threaded_baseline(oracle, inputs_mod, dt):
+    """The all-core CPU baseline (oracle_threaded.c): integers bit-identical to
+    the sequential oracle for any thread count and ragged chunking; floats
+    within the north_star tolerance of the sequential fp64 scan."""
+    kind = {"i32": inputs_mod.I32_FULL, "i8": inputs_mod.I8_FULL, "f32": inputs_mod.F32_NORMAL,
+            "f16": inputs_mod.F16_NORMAL}[dt]
+    for n in (1, 5, 1000, 100003):
+        x = inputs_mod.fill_host(kind, n, 0, n)
+        for T in (1, 2, 3, 8, 13):
+            for exc in (False, True):
+                got = oracle.scan_threaded(x, dt, exclusive=exc, threads=T)
+                ref = (oracle.exclusive if exc else oracle.inclusive)(x, dt)
+                if dt in ("i32", "i8"):
+                    assert np.array_equal(got, ref), (n, T, exc)
+                else:
+                    bad, worst, _ = oracle.check_f32(got, ref[0], ref[1])
+                    assert bad == 0, (n, T, exc, worst)
+                    if T == 1:
+                        assert np.array_equal(got, ref[2])
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32"])
+def test_threaded_rows_baseline(oracle, inputs_mod, dt):
+    """Row batches on T threads give exactly the sequential row oracle."""
+    kind = inputs_mod.I32_FULL if dt == "i32" else inputs_mod.F32_NORMAL
+    X = inputs_mod.fill_host(kind, 3, 0, 37 * 501).reshape(37, 501)
+    ref = oracle.rows(X, dt)
+    for T in (1, 4, 37, 64):
+        got = oracle.scan_threaded_rows(X, dt, threads=T)
+        assert np.array_equal(got, ref if dt == "i32" else ref[2]), T
