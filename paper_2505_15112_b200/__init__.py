@@ -137,7 +137,7 @@ class Workspace:
     queued there may still touch it."""
 
     def __init__(self, nbytes: int, device, stream=None):
-        nbytes = max(int(nbytes), 1 << 16)
+        nbytes = max(int(nbytes), 1 << 17)  # >= the header block (kWsDescOffset)
         s = stream if stream is not None else torch.cuda.current_stream(device)
         with torch.cuda.stream(s):
             self.buf = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)

@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
             Acc o[4];
             if constexpr (Tr::kFloat) {
                 const float P_hi = (float)P;
-                const float P_lo = (float)(P - (double)P_hi);
+                const float P_lo = isfinite(P_hi) ? (float)(P - (double)P_hi) : 0.f;  // inf carry: no inf - inf (R8)
                 const float base = P_lo + ((wpref + row_pref[j]) + lane_excl[j]);
                 if (p.exclusive) {
                     o[0] = P_hi + base;

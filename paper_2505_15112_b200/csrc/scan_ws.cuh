@@ -304,7 +304,7 @@ __global__ void __launch_bounds__((2 + NL + NC) * 32, 1) k_scan_ws(const ScanPar
             float P_hi = 0.f, base_f = 0.f;
             if constexpr (Tr::kFloat) {
                 P_hi = (float)P;
-                const float P_lo = (float)(P - (double)P_hi);
+                const float P_lo = isfinite(P_hi) ? (float)(P - (double)P_hi) : 0.f;  // inf carry: no inf - inf (R8)
                 base_f = P_lo + wpref;
             }
 #pragma unroll 4
