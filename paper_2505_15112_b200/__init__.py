@@ -27,7 +27,9 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libscan.so")
+# SCAN_LIB selects another in-tree build of the same library (the tests' stress
+# tier loads libscan_fuzz.so); a bare file name inside this package only.
+LIB_PATH = os.path.join(_HERE, os.path.basename(os.environ.get("SCAN_LIB", "libscan.so")))
 
 SCAN_I32_I32, SCAN_F32_F32, SCAN_F16_F32, SCAN_I8_I32 = 0, 1, 2, 3
 _STATUS = {0: "SCAN_OK", 1: "SCAN_ERR_ARG", 2: "SCAN_ERR_WORKSPACE", 3: "SCAN_ERR_CUDA",

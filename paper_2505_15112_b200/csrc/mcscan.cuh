@@ -1062,7 +1062,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         reinterpret_cast<unsigned long long*>(p.ws + kWsPartialsOffset)[blockIdx.x * kMcProf + tid] = s_prof[tid];
     if (tid == 0) {
         __threadfence();
-        const uint32_t prev = atomicAdd(&hdr->done, 1u);
+        const uint32_t prev = ptx::claim_add(&hdr->done, 1u);
         if (prev == gridDim.x - 1) {
             // every CTA is past every barrier: reset the counters for the next call
             for (int c = 0; c < gm.chunks; ++c) bar[c] = 0;

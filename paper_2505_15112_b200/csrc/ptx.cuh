@@ -13,6 +13,36 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p)
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// ---- fault injection (the T2 stress tier; libscan_fuzz.so only) ---------------
+// With -DSCAN_FUZZ every hand-off between warps, CTAs and the async proxy
+// (mbarrier arrivals, release arrivals on the grid barriers, look-back
+// descriptor publishes, ticket claims, bulk-store commits) first sleeps a
+// pseudo-random 0-4 us in about one call of four, so orderings that the normal
+// schedule never produces get exercised.  The product build compiles it away.
+#ifdef SCAN_FUZZ
+__device__ __forceinline__ void fuzz_delay(uint32_t site)
+{
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    uint32_t h = (uint32_t)(t ^ (t >> 23)) * 0x9E3779B1u;
+    h ^= blockIdx.x * 0x85EBCA6Bu ^ threadIdx.x * 0xC2B2AE35u ^ site * 0x27D4EB2Fu;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    if ((h & 3u) == 0) __nanosleep(h >> 20);
+}
+#define SCAN_FUZZ_POINT(site) ::scan::ptx::fuzz_delay(site)
+#else
+#define SCAN_FUZZ_POINT(site) ((void)0)
+#endif
+
+// A ticket / completion-counter claim (a fault-injection point in the fuzz build).
+__device__ __forceinline__ unsigned int claim_add(unsigned int* p, unsigned int v)
+{
+    SCAN_FUZZ_POINT(8);
+    return atomicAdd(p, v);
+}
+
 // ---- mbarrier ---------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
 {
@@ -27,6 +57,7 @@ __device__ __forceinline__ void fence_mbar_init()
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes)
 {
+    SCAN_FUZZ_POINT(1);
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
@@ -45,11 +76,13 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity)
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar)
 {
+    SCAN_FUZZ_POINT(2);
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t count)
 {
+    SCAN_FUZZ_POINT(3);
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 
@@ -117,7 +150,8 @@ __device__ __forceinline__ void tma_store_1d(void* gmem_dst, const void* smem_sr
                  : "memory");
 }
 
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_commit() {
+    SCAN_FUZZ_POINT(5); asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 
 // Wait until at most N committed bulk groups still READ shared memory.
 template <int N>
@@ -143,11 +177,13 @@ __device__ __forceinline__ void fence_proxy_async_smem()
 // ---- relaxed gpu-scope accesses for look-back descriptors -----------------------
 __device__ __forceinline__ void st_relaxed_u64(uint64_t* p, uint64_t v)
 {
+    SCAN_FUZZ_POINT(6);
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 __device__ __forceinline__ void st_relaxed_v2u64(uint64_t* p, uint64_t a, uint64_t b)
 {
+    SCAN_FUZZ_POINT(7);
     asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
@@ -180,6 +216,7 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p)
 // Release-ordered add without a return value (publish + arrive in one op).
 __device__ __forceinline__ void red_release_add_u32(uint32_t* p, uint32_t v)
 {
+    SCAN_FUZZ_POINT(4);
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 

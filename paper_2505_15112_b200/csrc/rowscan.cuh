@@ -122,7 +122,7 @@ __global__ void __launch_bounds__((2 + NC) * 32, 1) k_rowscan16(const __grid_con
             const uint64_t pol = ptx::policy_evict_first();
             int64_t q = 0;
             while (true) {
-                const int64_t row = (int64_t)atomicAdd(&hdr->ticket, 1u);
+                const int64_t row = (int64_t)ptx::claim_add(&hdr->ticket, 1u);
                 const bool end = row >= p.rows;
                 for (int k = 0; k < (end ? 1 : tpr); ++k, ++q) {
                     const int s = (int)(q % NB);
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__((2 + NC) * 32, 1) k_rowscan16(const __grid_con
     __syncthreads();
     if (tid == 0) {
         __threadfence();
-        const uint32_t prev = atomicAdd(&hdr->done, 1u);
+        const uint32_t prev = ptx::claim_add(&hdr->done, 1u);
         if (prev == gridDim.x - 1) {
             hdr->ticket = 0;
             hdr->done = 0;

@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
         if (p.static_sched) {
             t = (int64_t)blockIdx.x + q * gridDim.x;
         } else {
-            t = (int64_t)atomicAdd(&hdr->ticket, 1u);
+            t = (int64_t)ptx::claim_add(&hdr->ticket, 1u);
         }
         s_ticket[s] = t;
         int tma = 0;
@@ -692,7 +692,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
         ptx::bulk_wait<0>();  // all stores done before the CTA (and its smem) retires
         if (!p.static_sched) {
             __threadfence();
-            uint32_t prev = atomicAdd(&hdr->done, 1u);
+            uint32_t prev = ptx::claim_add(&hdr->done, 1u);
             if (prev == gridDim.x - 1) {
                 // Last CTA: every other CTA has claimed its final ticket and
                 // read the epoch.  Reset the counters and advance the epoch.
@@ -807,7 +807,7 @@ __global__ void __launch_bounds__(THREADS) k_total(const void* in_, int64_t n, v
         for (int w = 0; w < THREADS / 32; ++w) b += s_part[w];
         partials[blockIdx.x] = b;
         __threadfence();
-        uint32_t prev = atomicAdd(&hdr->total_done, 1u);
+        uint32_t prev = ptx::claim_add(&hdr->total_done, 1u);
         if (prev == gridDim.x - 1) {
             __threadfence();
             Sum t = 0;

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__((2 + NL + NC) * 32, 1) k_scan_ws(const ScanPar
                     else
                         mbar_wait_prof(&in_empty[s], (use - 1) & 1u, prof, &s_prof[6]);
                 }
-                int64_t t = (int64_t)atomicAdd(&hdr->ticket, 1u);
+                int64_t t = (int64_t)ptx::claim_add(&hdr->ticket, 1u);
                 if (t >= p.num_tiles) t = kEndTile;
                 s_tile_in[s] = t;
                 int tma = 0;
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__((2 + NL + NC) * 32, 1) k_scan_ws(const ScanPar
         reinterpret_cast<unsigned long long*>(p.ws + kWsPartialsOffset)[blockIdx.x * kNumProf + tid] = s_prof[tid];
     if (tid == 0) {
         __threadfence();
-        const uint32_t prev = atomicAdd(&hdr->done, 1u);
+        const uint32_t prev = ptx::claim_add(&hdr->done, 1u);
         if (prev == gridDim.x - 1) {
             hdr->ticket = 0;
             hdr->done = 0;

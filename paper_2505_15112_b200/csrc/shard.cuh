@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kThreads) k_block_sums(const void* in_, int64_
     // last CTA: exclusive scan of the block sums (fixed tree order), total
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    if (tid == 0) s_last = ptx::claim_add(done, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();

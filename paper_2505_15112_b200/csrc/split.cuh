@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kThreads) k_split_count(const SplitParams p)
     // last CTA: exclusive scan of the tile counts (fixed order, uint64 running total)
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&p.hdr[0], 1u) == gridDim.x - 1;
+    if (tid == 0) s_last = ptx::claim_add(&p.hdr[0], 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();

@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads) k_splitw_count(const WParams p)
     // last CTA: exclusive scan of the CTA totals
     __threadfence();
     __syncthreads();
-    if (tid == 0) s_last = atomicAdd(&p.hdr[0], 1u) == gridDim.x - 1;
+    if (tid == 0) s_last = ptx::claim_add(&p.hdr[0], 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(kSpThreads, 3) k_compress_sp(const WParams p, 
     const int nwt = (int)((p.n + kSpWT - 1) / kSpWT);
     for (;;) {
         int wt = 0;
-        if (lane == 0) wt = (int)atomicAdd(ticket, 1u);
+        if (lane == 0) wt = (int)ptx::claim_add(ticket, 1u);
         wt = __shfl_sync(0xffffffffu, wt, 0);
         if (wt >= nwt) break;
         const int64_t e0 = (int64_t)wt * kSpWT;

@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
 
     __shared__ int64_t s_row;
     for (;;) {
-        if (tid == 0) s_row = (int64_t)atomicAdd(ticket, 1u);
+        if (tid == 0) s_row = (int64_t)ptx::claim_add(ticket, 1u);
         __syncthreads();
         const int64_t row = s_row;
         __syncthreads();

@@ -46,9 +46,11 @@ KIND = {"i32": inputs.I32_FULL, "f32": inputs.F32_NORMAL, "f16": inputs.F16_NORM
 def main():
     torch.cuda.set_device(0)
     S.load()
+    print("library:", os.path.basename(S.LIB_PATH), flush=True)
     for dt in ("i32", "f32", "f16", "i8"):
         for n, tag in ((3000, "k_scan_tiles (one CTA)"), (60000, "k_scan_tiles (cluster)"),
-                       ((1 << 20) + 5, "k_mcscan16"), (100001, "k_scan_ws (look-back)")):
+                       ((1 << 20) + 5, "k_mcscan16"), ((1 << 24) + 7, "k_mcscan16 (multi-chunk)"),
+                       (100001, "k_scan_ws (look-back)")):
             x = inputs.fill_host(KIND[dt], n, 0, n + 1)
             xd = dev(x, dt)
             if "look-back" in tag:  # unaligned input
