@@ -784,8 +784,15 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         long long spin0 = 0;
         while (next_car < gm.chunks) {
             bool progressed = false;
-            if (next_pub < gm.chunks &&
-                ptx::mbar_try_wait(&rsum_ready[next_pub % RS], (uint32_t)(next_pub / RS) & 1u)) {
+            // lane 0's poll decides for the warp: every branch below must be
+            // warp-uniform (lanes polling on their own can disagree, and then
+            // the shuffles / __syncwarp further down diverge -- found by the
+            // fault-injection build, tests/test_gpu_fuzz.py)
+            bool rs_ready = false;
+            if (next_pub < gm.chunks && lane == 0)
+                rs_ready = ptx::mbar_try_wait(&rsum_ready[next_pub % RS], (uint32_t)(next_pub / RS) & 1u);
+            rs_ready = __shfl_sync(0xffffffffu, rs_ready, 0);
+            if (rs_ready) {
                 if (lane == 0) {
                     Carry t = Carry(0);
                     for (int w = 0; w < NC; ++w) t = t + s_job_sum[next_pub % RS][w];
@@ -844,6 +851,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                         s_carry[c % KC] = (lh_below < 0 ? chunk_carry : Carry(0)) + below;
                         ptx::mbar_arrive(&carry_ready[c % KC]);
                     }
+                    __syncwarp();
                     chunk_carry = (lh_all < 0 ? chunk_carry : Carry(0)) + total;
                     ++next_car;
                     progressed = true;

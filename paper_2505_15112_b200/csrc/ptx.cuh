@@ -20,8 +20,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p)
 // pseudo-random 0-4 us in about one call of four, so orderings that the normal
 // schedule never produces get exercised.  The product build compiles it away.
 #ifdef SCAN_FUZZ
+__device__ uint32_t g_fuzz_mask = 0xffffffffu;  // sites enabled (SCAN_FUZZ_MASK, set by the launcher)
+
 __device__ __forceinline__ void fuzz_delay(uint32_t site)
 {
+    if (((*(volatile uint32_t*)&g_fuzz_mask >> site) & 1u) == 0) return;
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     uint32_t h = (uint32_t)(t ^ (t >> 23)) * 0x9E3779B1u;

@@ -53,6 +53,12 @@ int dev_info(DevInfo& out)
         d.ok = (d.major == 10);
         cache[dev] = d;
         have[dev] = true;
+#ifdef SCAN_FUZZ
+        if (const char* m = getenv("SCAN_FUZZ_MASK")) {  // fault-injection sites to enable (stress build)
+            const uint32_t mask = (uint32_t)strtoul(m, nullptr, 0);
+            cudaMemcpyToSymbol(scan::ptx::g_fuzz_mask, &mask, sizeof(mask));
+        }
+#endif
     }
     out = cache[dev];
     return out.ok ? SCAN_OK : SCAN_ERR_DEVICE;

@@ -217,17 +217,22 @@ __global__ void __launch_bounds__((2 + NL + NC) * 32, 1) k_scan_ws(const ScanPar
         for (int64_t j = lw;; j += NL) {
             const int o = (int)(j % NB_OUT);
             const uint32_t par = (uint32_t)(j / NB_OUT) & 1u;
-            bool ended = false;
-            if (!ptx::mbar_try_wait(&local_done[o], par)) {
+            // lane 0 waits and decides for the warp (warp-uniform control flow
+            // for the collectives below); __syncwarp orders its acquire before
+            // the other lanes' shared-memory reads
+            int ended = 0;
+            if (lane == 0 && !ptx::mbar_try_wait(&local_done[o], par)) {
                 const long long w0 = prof ? clock64() : 0;
                 while (!ptx::mbar_try_wait(&local_done[o], par)) {
                     if (s_end <= j) {
-                        ended = true;
+                        ended = 1;
                         break;
                     }
                 }
-                if (prof && lane == 0) atomicAdd(&s_prof[3], (unsigned long long)(clock64() - w0));
+                if (prof) atomicAdd(&s_prof[3], (unsigned long long)(clock64() - w0));
             }
+            ended = __shfl_sync(0xffffffffu, ended, 0);
+            __syncwarp();
             if (ended) break;
             const int64_t t = s_tile_out[o];
             if (t == kEndTile) break;
