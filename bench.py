@@ -309,10 +309,20 @@ def cpu_baselines(cfg: str, seconds: float):
                             "sample": f"{sample1}; {t1:.1f} s of single-thread oracle (oracle_scan.c)"}}
 
 
+def allreduce_max(vals, dev):
+    """Max over ranks of a few host floats (NCCL: through the device)."""
+    import torch
+    import torch.distributed as dist
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor(vals, dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
 class Run:
     """One config on this rank: inputs in HBM, the step, its timing."""
 
-    def __init__(self, cfg, rank, world, dev):
+    def __init__(self, cfg, rank, world, dev, offset=0):
         import torch
 
         from paper_2505_15112_b200 import dist as D
@@ -325,6 +335,9 @@ class Run:
             lo, hi = D.shard_bounds(w["n"], world, rank)
             self.x = make_input(cfg, lo, hi - lo, dev)
             self.local_elems = hi - lo
+        elif offset and cfg != "C4":  # --offset K: the scan of x[K:], input off its 16-byte boundary
+            self.x = make_input(cfg, 0, w["n"] + offset, dev)[offset:]
+            self.local_elems = self.total_elems
         else:
             self.x = make_input(cfg, 0, w["rows"] if cfg == "C4" else w["n"], dev)
             self.local_elems = self.total_elems
@@ -421,9 +434,7 @@ class Run:
             kernel_ms = sum(a.elapsed_time(b) for a, b in ev_k) / steps
         if self.world > 1:
             vec = [ms, kernel_ms] + (list(phases.values()) if phases else [])
-            tt = torch.tensor(vec, dtype=torch.float64, device=self.dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            vals = tt.tolist()
+            vals = allreduce_max(vec, self.dev)
             ms, kernel_ms = vals[0], vals[1]
             if phases:
                 phases = dict(zip(PHASES, vals[2:]))
@@ -456,7 +467,8 @@ def run_ours(args, rank, world, local_rank):
 
     cfg = args.config
     w = WORK[cfg]
-    dev = torch.device("cuda", local_rank)
+    # --dist-backend gloo (harness test only): ranks may share a GPU
+    dev = torch.device("cuda", local_rank % max(1, torch.cuda.device_count()))
     torch.cuda.set_device(dev)
     S.load()
 
@@ -464,8 +476,8 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
-    run = Run(cfg, rank, world, dev)
-    m = run.measure(args.steps, args.warmup, args.graph, barrier, clocks=ClockSampler(local_rank))
+    run = Run(cfg, rank, world, dev, offset=args.offset)
+    m = run.measure(args.steps, args.warmup, args.graph, barrier, clocks=ClockSampler(dev.index))
     roof, value, ms_per_step = m["roof"], m["value"], m["ms_per_step"]
     peak = roof["peak"]
 
@@ -520,6 +532,8 @@ def run_ours(args, rank, world, local_rank):
             else "hot L2 (latency-bound size)",
             "cuda_graph": m["cuda_graph"],
         }
+        if args.offset:
+            config["input_offset_elements"] = args.offset
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
@@ -631,9 +645,7 @@ def run_e2e(args, run, dev, world, barrier):
     ms = a.elapsed_time(b)
     if world > 1:
         import torch.distributed as dist
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = t.item()
+        ms = allreduce_max([ms], dev)[0]
     h2d = x.numel() * x.element_size()
     d2h = out.numel() * out.element_size() * (2 if out2 is not None else 1)
     path = ("pinned host -> scan_host (C ABI: chunked H2D | scan | D2H on 3 streams) -> pinned host"
@@ -651,7 +663,7 @@ def relaunch(args) -> int:
 
     import torch
     have = torch.cuda.device_count()
-    if have < args.gpus:
+    if have < args.gpus and args.dist_backend == "nccl":
         log(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, this node has {have}")
         return 1
     s = socket.socket()
@@ -677,6 +689,10 @@ def main():
     ap.add_argument("--e2e-chunk", type=int, default=1 << 26, help="elements per host-streaming chunk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: test the multi-rank harness with ranks sharing one GPU (numbers not comparable)")
+    ap.add_argument("--offset", type=int, default=0,
+                    help="scan x[K:] of a K-longer array (input off its 16-byte boundary; 1-D configs)")
     ap.add_argument("--no-other-configs", action="store_true",
                     help="skip timing the other BASELINE.json configs after the main line")
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
@@ -701,8 +717,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:  # harness test on fewer GPUs than ranks: totals through host memory, no device waits
+            torch.cuda.set_device(local_rank % max(1, torch.cuda.device_count()))
+            dist.init_process_group("gloo")
     try:
         return run_ours(args, rank, world, local_rank)
     finally:

@@ -115,12 +115,17 @@ struct McParams16 {
     int exclusive;
     int debug;
     int ahead;              // reduce jobs run this many chunks ahead of scan jobs (1..4)
-    int l2;                 // L2 policies: bits 0-1 Phase-I read, bits 2-3 Phase-II re-read (0 = default)
+    int l2;                 // L2 policies: bits 0-1 Phase-I read, bits 2-3 Phase-II re-read (0 = default),
+                            // bits 4-5 after the re-read: 1 discard / 2 demote the tile's lines
     int64_t seg_len;        // > 0: segmented scan of contiguous rows of seg_len >= TILE elements
                             // (carries reset at every row start); 0: one 1-D scan
+    int shift;              // SHIFT instantiation: the input starts `shift` elements past a 16-byte
+                            // boundary; tm_in / the bulk copies address that aligned-down base
+    CUtensorMap tm_in1;     // SHIFT, 2-/4-byte inputs: the same view with a one-row box (the row
+                            // after a tile, which holds its last `shift` elements)
 };
 
-template <int DT, int NC, int GPW, int NB_IN, int NB_OUT>
+template <int DT, int NC, int GPW, int NB_IN, int NB_OUT, bool SHIFT = false>
 struct Mc16Cfg {
     using Tr = Traits<DT>;
     using In = typename Tr::In;
@@ -148,8 +153,17 @@ struct Mc16Cfg {
     // outputs are written in place over its input after the per-tile named
     // barrier, and the storer frees the slot once its store has read it.
     static constexpr bool kUni = NB_OUT == 0;
-    static constexpr size_t kRingSlot = kUni ? kOutSlot : kInSlot;
-    static constexpr size_t kSmem = kUni ? NB_IN * kOutSlot + 1024 : NB_IN * kInSlot + NB_OUT * kOutSlot + 1024;
+    // SHIFT: a tile also needs the 128-B row after it (its last `shift`
+    // elements).  1-byte inputs (linear slots): each slot is 128 B longer.
+    // 2-/4-byte inputs (swizzled slots): the extra rows sit together after the
+    // ring, row s for slot s, so every slot keeps its 1024-B swizzle phase.
+    static constexpr size_t kRingSlot = kUni ? kOutSlot : kInSlot + ((SHIFT && sizeof(In) == 1) ? 128 : 0);
+    static constexpr size_t up1k(size_t b) { return (b + 1023) & ~(size_t)1023; }
+    static constexpr size_t kExtraOff = up1k(NB_IN * kRingSlot);
+    static constexpr size_t kOutOff = kUni ? 0 : up1k(kExtraOff + ((SHIFT && sizeof(In) > 1) ? NB_IN * 128 : 0));
+    static constexpr size_t kSmem = kUni ? NB_IN * kOutSlot + 1024 : kOutOff + NB_OUT * kOutSlot + 1024;
+    static_assert(!(SHIFT && kUni), "shifted input needs a separate input ring");
+    static_assert(!SHIFT || NB_IN <= 8, "extra rows: one swizzle phase");
 };
 
 // ---- 16 contiguous elements of lane-offset e0 from a swizzled slot -----------
@@ -211,9 +225,22 @@ __device__ __forceinline__ uint32_t raw_bits(const void* p)
     else if constexpr (SZ == 2) return *reinterpret_cast<const uint16_t*>(p);
     else return *reinterpret_cast<const uint8_t*>(p);
 }
+// SHIFT, swizzled slots: byte address of slot position `pos` -- positions past
+// the tile (pos >= tile) live in the slot's extra row `xrow`, whose swizzle
+// phase is the slot index xs (extra rows are 128 B apart from a 1-KB boundary).
+template <int SZ>
+__device__ __forceinline__ const uint8_t* shift_elem(const uint8_t* slot, const uint8_t* xrow, int xs, int pos, int tile)
+{
+    if (SZ == 1 || pos < tile) return slot + swz_elem<SZ>(pos);
+    const int r = pos - tile;  // position within the extra row
+    constexpr int EPC = 16 / SZ;
+    return xrow + (((r / EPC) ^ xs) * 16) + (r % EPC) * SZ;
+}
+
 template <int SZ>
 __device__ __forceinline__ void grp_load_tail(const uint8_t* slot, const uint8_t* gin_tile, int e0, int m,
-                                              int m_tma, Grp<SZ>& g)
+                                              int m_tma, Grp<SZ>& g, int shift = 0, const uint8_t* xrow = nullptr,
+                                              int xs = 0, int tile = 1 << 30)
 {
 #pragma unroll
     for (int j = 0; j < 4 * SZ; ++j) g.w[j] = 0u;
@@ -221,7 +248,7 @@ __device__ __forceinline__ void grp_load_tail(const uint8_t* slot, const uint8_t
     for (int k = 0; k < 16; ++k) {
         const int e = e0 + k;
         uint32_t bits = 0u;
-        if (e < m_tma) bits = raw_bits<SZ>(slot + swz_elem<SZ>(e));
+        if (e < m_tma) bits = raw_bits<SZ>(shift_elem<SZ>(slot, xrow, xs, e + shift, tile));
         else if (e < m) bits = raw_bits<SZ>(gin_tile + (size_t)e * SZ);
         g.w[(k * SZ) / 4] |= bits << ((k * SZ * 8) & 31);
     }
@@ -472,6 +499,47 @@ __device__ __forceinline__ void grp_load_off(const uint8_t* base, const uint32_t
     }
 }
 
+// Full group of a SHIFTED slot: the lane's 16 elements sit at slot positions
+// e0 + d .. e0 + d + 15 (d = the input's element offset from a 16-byte
+// boundary, warp-uniform).  Loads the 16-byte chunks they touch (5 / 3 / 2 for
+// 4- / 2- / 1-byte elements, swizzled as the TMA wrote them) and funnel-shifts
+// the words into place.
+__device__ __forceinline__ uint32_t chunk_off(int q, int SZ)
+{
+    if (SZ == 1) return (uint32_t)q * 16;
+    const int R = q >> 3;
+    return (uint32_t)(R * 128 + ((q & 7) ^ (R & 7)) * 16);
+}
+// DW = whole words to skip (compile time: the word selection is register
+// renaming), sh = the remaining bit offset (0 / 8 / 16 / 24, one funnel shift
+// per word; always 0 for 4-byte elements).
+template <int SZ, int DW>
+__device__ __forceinline__ void grp_load_shift(const uint8_t* slot, int e0, uint32_t sh, Grp<SZ>& g,
+                                               const uint8_t* xrow, int xs, int tile)
+{
+    constexpr int EPC = 16 / SZ;              // elements per 16-byte chunk
+    constexpr int NQ = SZ == 4 ? 5 : (SZ == 2 ? 3 : 2);
+    uint32_t W[4 * NQ];
+    const int q0 = e0 / EPC;                  // e0 is a multiple of 16 elements
+    const int qt = tile / EPC;                // first chunk past the tile (swizzled slots: the extra row)
+#pragma unroll
+    for (int j = 0; j < NQ; ++j) {
+        const int q = q0 + j;
+        const uint8_t* a = (SZ > 1 && q >= qt) ? xrow + (((q - qt) ^ xs) * 16) : slot + chunk_off(q, SZ);
+        const uint4 v = *reinterpret_cast<const uint4*>(a);
+        W[4 * j] = v.x; W[4 * j + 1] = v.y; W[4 * j + 2] = v.z; W[4 * j + 3] = v.w;
+    }
+    constexpr int NW = 4 * SZ;                // words of the group
+    static_assert(DW + NW < 4 * NQ + 1, "chunks cover the shifted group");
+    if constexpr (SZ == 4) {
+#pragma unroll
+        for (int k = 0; k < NW; ++k) g.w[k] = W[DW + k];
+    } else {
+#pragma unroll
+        for (int k = 0; k < NW; ++k) g.w[k] = __funnelshift_r(W[DW + k], (DW + k + 1 < 4 * NQ) ? W[DW + k + 1] : 0u, sh);
+    }
+}
+
 template <typename A>
 __device__ __forceinline__ void store16_off(uint8_t* base, const uint32_t (&off)[4], const A (&o)[16])
 {
@@ -582,11 +650,15 @@ __device__ __forceinline__ typename Traits<DT>::Acc mc_split_tile(
 
 // SEG: segmented scan of contiguous rows (p.seg_len); a separate instantiation so
 // the 1-D kernels carry none of its code.
-template <int DT, int NC, int GPW, int NB_IN, int NB_OUT, bool SEG = false>
+// SH > 0: the input starts p.shift elements past a 16-byte boundary, with
+// (p.shift * sizeof(In)) / 4 == SH - 1 whole words (one instantiation each).
+template <int DT, int NC, int GPW, int NB_IN, int NB_OUT, bool SEG = false, int SH = 0>
 __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_constant__ McParams16 p)
 {
-
-    using Cfg = Mc16Cfg<DT, NC, GPW, NB_IN, NB_OUT>;
+    constexpr bool SHIFT = SH > 0;
+    constexpr int DW = SH > 0 ? SH - 1 : 0;
+    static_assert(!(SEG && SHIFT), "shifted input: 1-D scans only");
+    using Cfg = Mc16Cfg<DT, NC, GPW, NB_IN, NB_OUT, SHIFT>;
     using Tr = Traits<DT>;
     using In = typename Tr::In;
     using Out = typename Tr::Out;
@@ -602,7 +674,8 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     constexpr bool UNI = Cfg::kUni;
     constexpr int NSR = UNI ? NB_IN : NB_OUT;  // store_ready / out slots
     uint8_t* const in_ring = smem;
-    uint8_t* const out_ring = UNI ? smem : smem + NB_IN * Cfg::kInSlot;
+    uint8_t* const out_ring = UNI ? smem : smem + Cfg::kOutOff;
+    uint8_t* const extra_rows = smem + Cfg::kExtraOff;  // SHIFT, 2-/4-byte inputs: row s for slot s
 
     __shared__ __align__(8) uint64_t in_full[NB_IN];
     __shared__ __align__(8) uint64_t in_empty[NB_IN];
@@ -682,21 +755,28 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     if (rin.wrapped) ptx::mbar_wait(&in_empty[rin.s], rin.ph ^ 1u);
                     uint8_t* dst = in_ring + rin.s * Cfg::kRingSlot;
                     if constexpr (SZ == 1) {
+                        // SHIFT: bytes from the 16-byte boundary below the tile's first
+                        // element, up to 16 past its end (all 16-byte multiples)
                         const int64_t g0 = (int64_t)t * TILE;
-                        int64_t m_tma = p.n_tma_in - g0;
-                        m_tma = m_tma < 0 ? 0 : (m_tma > TILE ? TILE : m_tma);
+                        int64_t m_tma = p.n_tma_in + (SHIFT ? p.shift : 0) - g0;
+                        const int64_t cap = SHIFT ? TILE + 16 : TILE;
+                        m_tma = m_tma < 0 ? 0 : (m_tma > cap ? cap : m_tma);
                         if (m_tma > 0) {
                             ptx::mbar_arrive_expect_tx(&in_full[rin.s], (uint32_t)m_tma);
-                            ptx::tma_load_1d(dst, gin + g0, (uint32_t)m_tma, &in_full[rin.s], pol);
+                            ptx::tma_load_1d(dst, gin + g0 - (SHIFT ? p.shift : 0), (uint32_t)m_tma, &in_full[rin.s],
+                                             pol);
                         } else {
                             ptx::mbar_arrive(&in_full[rin.s]);
                         }
                     } else {
-                        ptx::mbar_arrive_expect_tx(&in_full[rin.s], (uint32_t)Cfg::kInSlot);
+                        ptx::mbar_arrive_expect_tx(&in_full[rin.s], (uint32_t)Cfg::kInSlot + (SHIFT ? 128u : 0u));
                         const int y0 = t * (TILE / Cfg::kRowElemsIn);
 #pragma unroll
                         for (int k = 0; k < Cfg::kBoxesIn; ++k)
                             tma_load_2d(dst + k * Cfg::kBoxRowsIn * 128, &p.tm_in, 0, y0 + Cfg::kBoxRowsIn * k,
+                                        &in_full[rin.s], pol);
+                        if constexpr (SHIFT)  // the row after the tile (its last `shift` elements)
+                            tma_load_2d(extra_rows + rin.s * 128, &p.tm_in1, 0, y0 + TILE / Cfg::kRowElemsIn,
                                         &in_full[rin.s], pol);
                     }
                 }
@@ -876,6 +956,11 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         const LaneOffsets<SZ> off(e0_base);
         constexpr uint32_t GI = LaneOffsets<SZ>::kGrpIn, GO = LaneOffsets<SZ>::kGrpOut;
         const uint8_t* const gin_b = reinterpret_cast<const uint8_t*>(p.in);
+        // L2 maintenance after the re-read (A/B, p.l2 bits 4-5); an in-place scan
+        // never discards (its output lands on the same lines)
+        int l2_after = (p.l2 >> 4) & 3;
+        const uint32_t sh_bits = (uint32_t)((p.shift * SZ) & 3) * 8;  // SHIFT: bits past the DW words
+        if (l2_after == 1 && p.in == (const void*)p.out) l2_after = 2;
         const bool exclusive = p.exclusive != 0;
         const bool prof0 = prof && cw == 0 && lane == 0;
         Ring<NB_IN> rin;
@@ -922,7 +1007,11 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
 #pragma unroll
                         for (int g = 0; g < GPW; ++g) {
                             Grp<SZ> gr;
-                            grp_load_off(slot + g * GI, off.in, gr);
+                            if (SHIFT && !(p.debug & 8))
+                                grp_load_shift<SZ, DW>(slot, e0_base + 512 * g, sh_bits, gr,
+                                                       extra_rows + rin.s * 128, rin.s, TILE);
+                            else
+                                grp_load_off(slot + g * GI, off.in, gr);
                             jsum = jsum + Carry(grp_sum(gr, (const In*)nullptr));
                         }
                     } else {
@@ -931,7 +1020,8 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
 #pragma unroll
                         for (int g = 0; g < GPW; ++g) {
                             Grp<SZ> gr;
-                            grp_load_tail(slot, gin_b + (int64_t)t * TILE * SZ, e0_base + 512 * g, m, m_in, gr);
+                            grp_load_tail(slot, gin_b + (int64_t)t * TILE * SZ, e0_base + 512 * g, m, m_in, gr,
+                                          SHIFT ? p.shift : 0, extra_rows + rin.s * 128, rin.s, TILE);
                             jsum = jsum + Carry(grp_sum(gr, (const In*)nullptr));
                         }
                     }
@@ -987,16 +1077,33 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     Acc wsum = Acc(0);
 #pragma unroll
                     for (int g = 0; g < GPW; ++g) {
-                        if (full)
+                        if (full && SHIFT && !(p.debug & 8))  // debug bit 3: unshifted loads (timing only)
+                            grp_load_shift<SZ, DW>(slot, e0_base + 512 * g, sh_bits, ls[g].g, extra_rows + s * 128,
+                                                   s, TILE);
+                        else if (full)
                             grp_load_off(slot + g * GI, off.in, ls[g].g);
                         else
                             grp_load_tail(slot, gin_b + (int64_t)t * TILE * SZ, e0_base + 512 * g, m, m_in,
-                                          ls[g].g);
+                                          ls[g].g, SHIFT ? p.shift : 0, extra_rows + s * 128, s, TILE);
                         ex[g] = ls[g].prefix();  // lane total (held in ex until the shuffle scan)
                     }
                     if (!UNI) {  // unified ring: the storer frees the slot after the store
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive(&in_empty[s]);
+                    }
+                    if (l2_after && full) {
+                        // the re-read was this tile's last use of its input: release its
+                        // L2 lines (one 128-byte line per compute thread) so the lines of
+                        // the chunks still waiting for their re-read stay resident
+                        const uintptr_t tb = (uintptr_t)(gin_b + (int64_t)t * TILE * SZ);
+                        const uintptr_t a1 = (tb + (uintptr_t)TILE * SZ) & ~(uintptr_t)127;
+                        for (uintptr_t a = ((tb + 127) & ~(uintptr_t)127) + (uintptr_t)(cw * 32 + lane) * 128; a < a1;
+                             a += (uintptr_t)NC * 32 * 128) {
+                            if (l2_after == 1)
+                                ptx::l2_discard_line(reinterpret_cast<const void*>(a));
+                            else
+                                ptx::l2_demote_line(reinterpret_cast<const void*>(a));
+                        }
                     }
 #pragma unroll
                     for (int g = 0; g < GPW; ++g) {

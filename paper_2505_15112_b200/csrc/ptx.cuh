@@ -125,6 +125,17 @@ __device__ __forceinline__ uint64_t policy_evict_unchanged()
 }
 
 // evict_last on `fraction` of the accessed lines, priority unchanged on the rest
+// L2 line maintenance after a line's last use: drop it (clean input only: the
+// line's contents become undefined) or demote it to normal eviction priority.
+__device__ __forceinline__ void l2_discard_line(const void* p128)
+{
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p128) : "memory");
+}
+__device__ __forceinline__ void l2_demote_line(const void* p128)
+{
+    asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(p128) : "memory");
+}
+
 __device__ __forceinline__ uint64_t policy_evict_last_frac(float fraction)
 {
     uint64_t pol;

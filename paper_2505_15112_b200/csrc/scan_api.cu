@@ -282,7 +282,8 @@ int env_int(const char* name, int dflt)
     return e ? atoi(e) : dflt;
 }
 
-constexpr int kMaxGrid = 192;  // workspace sizing bound on the CTA count (B200: 148)
+constexpr int kMaxGrid = 192;
+constexpr size_t kWsHeadCarry = 208;  // header pad: the body carry of an unaligned 1-D scan (8 B)  // workspace sizing bound on the CTA count (B200: 148)
 constexpr int64_t kMcMinElems = 1 << 20;  // below this the look-back kernel wins (one chunk)
 
 // ---- TMA tensor maps (driver entry point, no libcuda link dependency) ----------
@@ -319,9 +320,10 @@ bool encode_rows128(CUtensorMap* tm, const void* base, int64_t rows, int elem_by
 }
 
 // Second-generation MCScan: 16 contiguous elements per lane (mcscan16.cuh).
-template <int DT, int NC, int GPW, int NBI, int NBO, bool SEG = false>
+template <int DT, int NC, int GPW, int NBI, int NBO, bool SEG = false, int SH = 0>
 struct Mc16Variant {
-    using Cfg = Mc16Cfg<DT, NC, GPW, NBI, NBO>;
+    static constexpr bool SHIFT = SH > 0;
+    using Cfg = Mc16Cfg<DT, NC, GPW, NBI, NBO, SHIFT>;
     static constexpr int kTile = Cfg::kTile;
 
     // segmented: sp's contiguous rows as one segmented scan (row length a whole
@@ -337,7 +339,7 @@ struct Mc16Variant {
         static DevOnce once;
         static cudaError_t err = cudaSuccess;
         dev_call_once(once, [] {
-            err = cudaFuncSetAttribute(k_mcscan16<DT, NC, GPW, NBI, NBO, SEG>,
+            err = cudaFuncSetAttribute(k_mcscan16<DT, NC, GPW, NBI, NBO, SEG, SH>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
         });
         if (err != cudaSuccess) return SCAN_ERR_CUDA;
@@ -346,12 +348,18 @@ struct Mc16Variant {
         const int64_t n = segmented ? sp.seg_len * sp.num_segs : sp.seg_len;
         const int64_t rows_out = n / 32;
         if (!encode_rows128(&p.tm_out, sp.out, rows_out, 4, Cfg::kBoxRowsOut)) return SCAN_ERR_CUDA;
+        // SHIFT: the input views start at the 16-byte boundary `d` elements below
+        // `in`; n_tma_in counts the elements of `in` those views cover
+        const int d = SHIFT ? sp.shift : 0;
+        const void* in_al = (const uint8_t*)sp.in - (int64_t)d * (int64_t)sizeof(In);
+        p.shift = d;
         if constexpr (sizeof(In) == 1) {
-            p.n_tma_in = n & ~(int64_t)15;
+            p.n_tma_in = ((n + d) & ~(int64_t)15) - d;
         } else {
-            const int64_t rows_in = n / Cfg::kRowElemsIn;
-            if (!encode_rows128(&p.tm_in, sp.in, rows_in, (int)sizeof(In), Cfg::kBoxRowsIn)) return SCAN_ERR_CUDA;
-            p.n_tma_in = rows_in * Cfg::kRowElemsIn;
+            const int64_t rows_in = (n + d) / Cfg::kRowElemsIn;
+            if (!encode_rows128(&p.tm_in, in_al, rows_in, (int)sizeof(In), Cfg::kBoxRowsIn)) return SCAN_ERR_CUDA;
+            if (SHIFT && !encode_rows128(&p.tm_in1, in_al, rows_in, (int)sizeof(In), 1)) return SCAN_ERR_CUDA;
+            p.n_tma_in = rows_in * Cfg::kRowElemsIn - d;
         }
         p.n_tma_out = rows_out * 32;
         p.in = sp.in;
@@ -378,7 +386,7 @@ struct Mc16Variant {
         p.gm.chunk_tiles = p.gm.g * p.gm.bt;
         p.gm.chunks = (int)((ntiles + p.gm.chunk_tiles - 1) / p.gm.chunk_tiles);
         void* args[] = {&p};
-        cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_mcscan16<DT, NC, GPW, NBI, NBO, SEG>,
+        cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_mcscan16<DT, NC, GPW, NBI, NBO, SEG, SH>,
                                                     dim3(p.gm.g), dim3(Cfg::kThreads), args, Cfg::kSmem, s);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return e == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
@@ -416,10 +424,41 @@ int launch_mc_sized(const ScanParams& p, cudaStream_t s, const DevInfo& di)
 // Default variant per dtype (warps, groups per warp, input slots, output slots;
 // 0 output slots = outputs in place in the input ring); SCAN_MC selects
 // alternatives for tuning runs.
+// Shifted-input MCScan (default warp / ring configuration): one instantiation
+// per whole-word part of the shift, SH - 1 = (shift * sizeof(In)) / 4.
+template <int DT, int SH>
+int launch_mc_shift_sh(const ScanParams& p, cudaStream_t s, const DevInfo& di)
+{
+    constexpr bool wide_in = (DT == SCAN_I32_I32 || DT == SCAN_F32_F32);
+    if constexpr (wide_in && SH == 1) {
+        return SCAN_ERR_ARG;  // 4-byte elements: a nonzero shift is >= 1 whole word
+    } else if constexpr (wide_in) {
+        return launch_mc_sized<Mc16Variant<DT, 12, 2, 3, 1, false, SH>, DT>(p, s, di);
+    } else if constexpr (DT == SCAN_F16_F32) {  // one input slot fewer: the extra rows must fit
+        return launch_mc_sized<Mc16Variant<DT, 16, 2, 2, 2, false, SH>, DT>(p, s, di);
+    } else {
+        return launch_mc_sized<Mc16Variant<DT, 16, 2, 5, 2, false, SH>, DT>(p, s, di);
+    }
+}
+
+template <int DT>
+int launch_mc_shift(const ScanParams& p, cudaStream_t s, const DevInfo& di)
+{
+    using In = typename Traits<DT>::In;
+    switch ((p.shift * (int)sizeof(In)) >> 2) {
+    case 0: return launch_mc_shift_sh<DT, 1>(p, s, di);
+    case 1: return launch_mc_shift_sh<DT, 2>(p, s, di);
+    case 2: return launch_mc_shift_sh<DT, 3>(p, s, di);
+    default: return launch_mc_shift_sh<DT, 4>(p, s, di);
+    }
+}
+
 template <int DT>
 int launch_mc(const ScanParams& p, cudaStream_t s, const DevInfo& di)
 {
     constexpr bool wide_in = (DT == SCAN_I32_I32 || DT == SCAN_F32_F32);
+    if (p.shift != 0)  // input not on a 16-byte boundary (the output is): shifted slots
+        return launch_mc_shift<DT>(p, s, di);
     switch (env_int("SCAN_MC", 0)) {
     case 1:
         if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 2, 2, 1>, DT>(p, s, di);
@@ -760,6 +799,38 @@ int scan_1d(const void* in, void* out, int64_t n, int dt, const void* carry_in, 
     p.tma_in = ((uintptr_t)in & 15u) == 0;
     p.tma_out = ((uintptr_t)out & 15u) == 0;
     if ((st = ws_clean(ws, ws_bytes, (cudaStream_t)stream)) != SCAN_OK) return st;
+    if (!(p.tma_in && p.tma_out) && n >= kMcMinElems + 16 && ((uintptr_t)out & 3u) == 0 &&
+        ((uintptr_t)in % in_size(dt)) == 0 && variant() == 0 && env_int("SCAN_NO_MC", 0) == 0 &&
+        env_int("SCAN_NO_SHIFT", 0) == 0) {
+        // Unaligned 1-D array: the <= 3-element head up to the output's next 16-byte
+        // boundary is scanned on its own (k_scan_head: head outputs, and carry_in +
+        // head sum into the workspace header), then the MCScan runs on the rest with
+        // an aligned output and, if the input is still off a 16-byte boundary, the
+        // shifted-slot instantiation (its TMA views start at the boundary below).
+        const int h = (int)(((16u - ((uintptr_t)out & 15u)) & 15u) / 4u);
+        cudaStream_t s = (cudaStream_t)stream;
+        const void* carry = carry_in;
+        if (h > 0) {
+            void* slot = (uint8_t*)ws + kWsHeadCarry;
+            switch (dt) {
+            case SCAN_I32_I32: k_scan_head<0><<<1, 32, 0, s>>>(in, out, h, carry_in, exclusive, slot); break;
+            case SCAN_F32_F32: k_scan_head<1><<<1, 32, 0, s>>>(in, out, h, carry_in, exclusive, slot); break;
+            case SCAN_F16_F32: k_scan_head<2><<<1, 32, 0, s>>>(in, out, h, carry_in, exclusive, slot); break;
+            default: k_scan_head<3><<<1, 32, 0, s>>>(in, out, h, carry_in, exclusive, slot); break;
+            }
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+            if (cudaGetLastError() != cudaSuccess) return SCAN_ERR_CUDA;
+            carry = slot;
+        }
+        const uint8_t* body_in = (const uint8_t*)in + (int64_t)h * (int64_t)in_size(dt);
+        p.in = body_in;
+        p.out = (uint8_t*)out + (int64_t)h * 4;
+        p.seg_len = p.in_stride = p.out_stride = n - h;
+        p.carry_in = carry;
+        p.tma_in = p.tma_out = 1;
+        p.shift = (int)(((uintptr_t)body_in & 15u) / in_size(dt));
+        return launch_any(dt, p, s, di);
+    }
     return launch_any(dt, p, (cudaStream_t)stream, di);
 }
 

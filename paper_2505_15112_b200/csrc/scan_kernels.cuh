@@ -391,6 +391,7 @@ struct ScanParams {
     int cluster;            // > 0: small-n mode, one tile per CTA of ONE cluster, carries via DSMEM
     int debug;              // bit 0: skip look-back (timing only; wrong results); bit 1: spin without
                             // nanosleep; bit 2: per-CTA stall counters into the workspace
+    int shift;              // MCScan SHIFT: `in` is this many elements past a 16-byte boundary
 };
 
 template <int THREADS, int ROWS>
@@ -826,6 +827,50 @@ __global__ void k_carry_from_totals(const Sum* totals, int rank, Sum* carry_out)
         Sum c = 0;
         for (int r = 0; r < rank; ++r) c += totals[r];
         *carry_out = c;
+    }
+}
+
+// The <= 15-element head of a 1-D scan whose output is not 16-byte aligned
+// (scan_1d then runs the MCScan on the aligned rest): one thread scans it
+// sequentially from carry_in (P68 / P461) and leaves carry_in + sum(head) in
+// *carry_out (int64 / fp64, the carry_in type) for the body.
+template <int DT>
+__global__ void k_scan_head(const void* in, void* out, int h, const void* carry_in, int exclusive, void* carry_out)
+{
+    using Tr = Traits<DT>;
+    using In = typename Tr::In;
+    using Out = typename Tr::Out;
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const In* x = reinterpret_cast<const In*>(in);
+    Out* y = reinterpret_cast<Out*>(out);
+    if constexpr (Tr::kFloat) {
+        double c = carry_in ? *reinterpret_cast<const double*>(carry_in) : 0.0;
+        for (int i = 0; i < h; ++i) {
+            double xi;
+            if constexpr (sizeof(In) == 2) xi = (double)__half2float(__ushort_as_half(x[i]));  // raw binary16 bits
+            else xi = (double)x[i];
+            if (exclusive) {
+                y[i] = (float)c;
+                c = c + xi;
+            } else {
+                c = (i == 0 && !carry_in) ? xi : c + xi;
+                y[i] = (float)c;
+            }
+        }
+        *reinterpret_cast<double*>(carry_out) = c;
+    } else {
+        uint32_t c = carry_in ? (uint32_t)(uint64_t)*reinterpret_cast<const int64_t*>(carry_in) : 0u;
+        for (int i = 0; i < h; ++i) {
+            const uint32_t xi = (uint32_t)(int32_t)x[i];
+            if (exclusive) {
+                y[i] = (int32_t)c;
+                c += xi;
+            } else {
+                c += xi;
+                y[i] = (int32_t)c;
+            }
+        }
+        *reinterpret_cast<int64_t*>(carry_out) = (int64_t)(int32_t)c;
     }
 }
 

@@ -255,7 +255,7 @@ __device__ __forceinline__ void warp_first_level(const double* lvl, const unsign
 // The counter lives in the caller's workspace header (the launcher zeroes it on
 // the stream before the launch), so concurrent or graph-captured calls with
 // distinct workspaces never share it.
-constexpr size_t kTicketWsOffset = 192;  // inside the 256-byte workspace header pad
+constexpr size_t kTicketWsOffset = 200;  // inside the 256-byte workspace header pad (192: shard counter)
 
 __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64_t rows, int64_t cols, int64_t stride,
                                                     float p, const float* u, int64_t* token_out, int32_t* kept_out,

@@ -50,10 +50,10 @@ def main():
     for dt in ("i32", "f32", "f16", "i8"):
         for n, tag in ((3000, "k_scan_tiles (one CTA)"), (60000, "k_scan_tiles (cluster)"),
                        ((1 << 20) + 5, "k_mcscan16"), ((1 << 24) + 7, "k_mcscan16 (multi-chunk)"),
-                       (100001, "k_scan_ws (look-back)")):
+                       (100001, "k_scan_ws (look-back)"), ((1 << 21) + 9, "k_scan_head + k_mcscan16 SHIFT")):
             x = inputs.fill_host(KIND[dt], n, 0, n + 1)
             xd = dev(x, dt)
-            if "look-back" in tag:  # unaligned input
+            if "look-back" in tag or "SHIFT" in tag:  # unaligned input
                 xd, x = xd[1:], x[1:]
             else:
                 xd, x = xd[:n], x[:n]

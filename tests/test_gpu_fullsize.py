@@ -39,8 +39,8 @@ def test_c1_full(cuda, oracle, inputs_mod):
     assert np.array_equal(cuda.exclusive(x).cpu().numpy(), oracle.exclusive(xh, "i32"))
 
 
-def _stream_check(cuda, oracle, inputs_mod, kind, seed, n, dtype, dt, exclusive, every=1):
-    x = _device_input(inputs_mod, kind, seed, n, dtype)
+def _stream_check(cuda, oracle, inputs_mod, kind, seed, n, dtype, dt, exclusive, every=1, offset=0):
+    x = _device_input(inputs_mod, kind, seed, n + offset, dtype)[offset:]
     y = (cuda.exclusive if exclusive else cuda.inclusive)(x)
     torch.cuda.synchronize()
     del x
@@ -48,7 +48,7 @@ def _stream_check(cuda, oracle, inputs_mod, kind, seed, n, dtype, dt, exclusive,
     worst, checked = 0.0, 0
     for k, lo in enumerate(range(0, n, CHUNK)):
         cnt = min(CHUNK, n - lo)
-        xh = inputs_mod.fill_host(kind, seed, lo, cnt)
+        xh = inputs_mod.fill_host(kind, seed, lo + offset, cnt)
         last = lo + cnt >= n
         if k % every and not last:
             st(xh, exclusive) if dt in ("i32", "i8") else st(xh, exclusive, want64=False, want_abs=False,
@@ -96,3 +96,16 @@ def test_c5_full(cuda, oracle, inputs_mod):
     worst, checked = _stream_check(cuda, oracle, inputs_mod, inputs_mod.F32_NORMAL, 4, 1 << 32, torch.float32,
                                    "f32", False)
     assert checked == (1 << 32) // CHUNK and worst < 0.5
+
+
+def test_c3_unaligned_full(cuda, oracle, inputs_mod):
+    """C3 on x[1:] (input one byte past a 16-byte boundary, fresh aligned output):
+    the shifted-slot MCScan, every element bit-exact."""
+    _stream_check(cuda, oracle, inputs_mod, inputs_mod.I8_FLAG, 2, (1 << 30) - 1, torch.int8, "i8", True, offset=1)
+
+
+def test_c2_unaligned_full(cuda, oracle, inputs_mod):
+    """C2 on x[3:] (fp16 input 6 bytes past a boundary): shifted-slot MCScan."""
+    worst, _ = _stream_check(cuda, oracle, inputs_mod, inputs_mod.F16_U01, 1, (1 << 28) - 3, torch.float16, "f16",
+                             False, offset=3)
+    assert worst < 0.5
