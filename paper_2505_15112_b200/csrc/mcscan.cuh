@@ -522,11 +522,17 @@ __device__ __forceinline__ void grp_load_shift(const uint8_t* slot, int e0, uint
     uint32_t W[4 * NQ];
     const int q0 = e0 / EPC;                  // e0 is a multiple of 16 elements
     const int qt = tile / EPC;                // first chunk past the tile (swizzled slots: the extra row)
+    // 32-bit shared-window addresses and explicit ld.shared.v4 (a select between
+    // two generic pointers made the compiler fall back to split generic loads)
+    const uint32_t s_slot = ptx::smem_u32(slot), s_x = ptx::smem_u32(xrow);
 #pragma unroll
     for (int j = 0; j < NQ; ++j) {
         const int q = q0 + j;
-        const uint8_t* a = (SZ > 1 && q >= qt) ? xrow + (((q - qt) ^ xs) * 16) : slot + chunk_off(q, SZ);
-        const uint4 v = *reinterpret_cast<const uint4*>(a);
+        const uint32_t a = (SZ > 1 && q >= qt) ? s_x + (uint32_t)(((q - qt) ^ xs) * 16) : s_slot + chunk_off(q, SZ);
+        uint4 v;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "r"(a));
         W[4 * j] = v.x; W[4 * j + 1] = v.y; W[4 * j + 2] = v.z; W[4 * j + 3] = v.w;
     }
     constexpr int NW = 4 * SZ;                // words of the group
