@@ -38,6 +38,8 @@ OPS = {
                      n=1 << 28),
     "top_p": dict(name="top-p sampling: 4096 rows x 131072 softmax(4*N(0,1)) fp32 (C4 rows), p=0.9, "
                        "row sort + row scan + nucleus draw", n=4096 * 131072),
+    "sort_rows": dict(name="row-batched LSB radix sort, descending stable: 4096 rows x 131072 softmax(4*N(0,1)) "
+                           "fp32 (C4 rows) + int32 column indices (the top-p sort path's sort)", n=4096 * 131072),
 }
 
 
@@ -61,6 +63,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=5.0)
+    ap.add_argument("--top-p-method", choices=["select", "sort"], default="select")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -105,6 +108,17 @@ def main():
         alg = passes * n * (2 + 2 + 4 + 4) - n * 4
         ref_fn = lambda: torch.sort(k, stable=True)  # noqa: E731
         ref_name = "torch.sort(stable=True) (CUB radix sort, int64 indices)"
+    elif args.op == "sort_rows":
+        R, C = 4096, 131072
+        k = torch.empty((R, C), dtype=torch.float32, device=dev)
+        inputs.fill_device(inputs.F32_SOFTMAX, 3, 0, R, C, k)
+        ko = torch.empty_like(k)
+        idx = torch.empty((R, C), dtype=torch.int32, device=dev)
+        fn = lambda: S.radix_sort_rows(k, descending=True, out=ko, idx_out=idx)  # noqa: E731
+        # 4 passes of 8-bit digits: keys in + out, indices in + out (pass 0 reads none)
+        alg = 4 * n * (4 + 4 + 4 + 4) - n * 4
+        ref_fn = lambda: torch.sort(k, dim=1, descending=True, stable=True)  # noqa: E731
+        ref_name = "torch.sort(dim=1, descending=True, stable=True) (CUB segmented sort, int64 indices)"
     elif args.op == "weighted":
         wgt = torch.empty(n, dtype=torch.float32, device=dev)
         inputs.fill_device(inputs.F32_NORMAL, 6, 0, n, 0, wgt)
@@ -119,7 +133,7 @@ def main():
         probs = torch.empty((R, C), dtype=torch.float32, device=dev)
         inputs.fill_device(inputs.F32_SOFTMAX, 3, 0, R, C, probs)
         uu = torch.rand(R, generator=torch.Generator(device=dev).manual_seed(7), device=dev)
-        fn = lambda: S.top_p_sample(probs, 0.9, uu)  # noqa: E731
+        fn = lambda: S.top_p_sample(probs, 0.9, uu, method=args.top_p_method)  # noqa: E731
         alg = R * C * 4  # bytes of probabilities consumed per step
 
         def ref_fn():
@@ -142,8 +156,18 @@ def main():
 
     # cpu_baseline: the oracle as it stands on a bounded sample of the same workload
     import oracle
-    cn = 1 << 22 if args.op != "sort" else 1 << 18
-    if args.op == "top_p":
+    cn = 1 << 22 if args.op not in ("sort", "sort_rows") else 1 << 18
+    if args.op == "sort_rows":
+        cn = 131072
+        Ph = inputs.fill_host(inputs.F32_SOFTMAX, 3, 0, 1, cn)[0]
+        t0 = time.perf_counter()
+        reps = 0
+        while time.perf_counter() - t0 < args.cpu_seconds:
+            oracle.radix_sort(Ph, "f32", descending=True)
+            reps += 1
+        ct = time.perf_counter() - t0
+        cpu_alg = alg / n * cn * reps
+    elif args.op == "top_p":
         cn = 131072
         Ph = inputs.fill_host(inputs.F32_SOFTMAX, 3, 0, 1, C)[0]
         t0 = time.perf_counter()
@@ -187,9 +211,11 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": {"split": "fp16 payload / int8 mask / int32 indices", "compress": "fp16 payload / int8 mask",
                   "sort": "fp16 keys / int32 indices", "weighted": "f32 (fp64 carry)",
-                  "top_p": "f32 probabilities / int64 tokens"}[args.op],
+                  "top_p": "f32 probabilities / int64 tokens",
+                  "sort_rows": "f32 keys / int32 column indices"}[args.op],
         "data": "synthetic (seeded counter-based generator, inputs/recipe.h; generated in HBM)",
-        "config": {"workload": w["name"], "n_elements": n, "alg_bytes_per_step": alg,
+        "config": {"workload": w["name"] + (f" [method={args.top_p_method}]" if args.op == "top_p" else ""),
+                   "n_elements": n, "alg_bytes_per_step": alg,
                    "gelem_per_s": round(n / med / 1e9, 2),
                    "l2_flush": "not needed: inputs exceed the 126 MB L2"},
         "roofline": {"bound": "hbm", "achieved": round(value, 1), "peak": peak, "unit": "GB/s",

@@ -87,6 +87,22 @@ SCAN_API size_t scan_radix_sort_workspace_bytes(int64_t n, int key_type);
 SCAN_API int scan_radix_sort(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, int key_type,
                              int descending, void* ws, size_t ws_bytes, void* stream);
 
+/* Row-batched LSB radix sort: each of the `rows` rows of `cols` contiguous keys
+ * (keys + r*cols) is sorted on its own -- the sort of P299's top-p pipeline
+ * ("applies sort and scan on the token probability vector"), by the same 8-bit
+ * digit passes as scan_radix_sort.  Per pass the per-(row, digit, tile) counts
+ * are laid out [row][digit][tile] and ONE exclusive row scan per row
+ * (scan_rows, P437) gives every (digit, tile) its start inside the row.
+ * keys_out [rows*cols] the sorted rows; idx_out [rows*cols] int32 COLUMN index
+ * (within the row) of every sorted key.  Stable; descending != 0: descending,
+ * equal keys still in ascending column order (= torch.sort(descending=True,
+ * stable=True)).  Key order as scan_radix_sort (R13).  ws:
+ * scan_radix_sort_rows_workspace_bytes(rows, cols, key_type) bytes, 256-byte
+ * aligned; cols < 2^31.  Errors as scan_radix_sort. */
+SCAN_API size_t scan_radix_sort_rows_workspace_bytes(int64_t rows, int64_t cols, int key_type);
+SCAN_API int scan_radix_sort_rows(const void* keys, void* keys_out, int32_t* idx_out, int64_t rows, int64_t cols,
+                                  int key_type, int descending, void* ws, size_t ws_bytes, void* stream);
+
 /* Weighted sampling (P463).  w [n] fp32 non-negative weights with a positive
  * sum; cdf [n] fp32 device scratch that receives the inclusive scan; ws a scan
  * workspace of scan_workspace_bytes(SCAN_F32_F32, n) bytes; index_out ONE
@@ -96,11 +112,11 @@ SCAN_API int scan_weighted_sample(const float* w, int64_t n, double theta, int64
 
 /* Top-p draw on `rows` rows.  cdf: row r at cdf + r*cdf_row_stride, the
  * inclusive scan of row r's probabilities sorted in descending order; order:
- * row r at order + r*order_row_stride, int64 original column of every sorted
- * entry; u [rows] fp32 uniform draws in [0, 1); p the nucleus mass.
- * Outputs: token_out [rows] int64 sampled column, kept_out NULL or [rows]
- * int32 nucleus size K.  Strides are in elements, >= cols. */
-SCAN_API int scan_top_p_draw(const float* cdf, const int64_t* order, int64_t rows, int64_t cols,
+ * row r at order + r*order_row_stride, int32 original column of every sorted
+ * entry (scan_radix_sort_rows' idx_out); u [rows] fp32 uniform draws in [0, 1);
+ * p the nucleus mass.  Outputs: token_out [rows] int64 sampled column, kept_out
+ * NULL or [rows] int32 nucleus size K.  Strides are in elements, >= cols. */
+SCAN_API int scan_top_p_draw(const float* cdf, const int32_t* order, int64_t rows, int64_t cols,
                              int64_t cdf_row_stride, int64_t order_row_stride, float p, const float* u,
                              int64_t* token_out, int32_t* kept_out, void* stream);
 

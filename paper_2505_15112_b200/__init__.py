@@ -104,6 +104,10 @@ def load() -> ctypes.CDLL:
         L.scan_radix_sort_workspace_bytes.restype = SZ
         L.scan_radix_sort.argtypes = [P, P, P, I64, I, I, P, SZ, P]
         L.scan_radix_sort.restype = I
+        L.scan_radix_sort_rows_workspace_bytes.argtypes = [I64, I64, I]
+        L.scan_radix_sort_rows_workspace_bytes.restype = SZ
+        L.scan_radix_sort_rows.argtypes = [P, P, P, I64, I64, I, I, P, SZ, P]
+        L.scan_radix_sort_rows.restype = I
         L.scan_weighted_sample.argtypes = [P, I64, ctypes.c_double, P, P, P, SZ, P]
         L.scan_weighted_sample.restype = I
         L.scan_top_p_draw.argtypes = [P, P, I64, I64, I64, I64, ctypes.c_float, P, P, P, P]
@@ -405,6 +409,25 @@ def radix_sort(keys: torch.Tensor, descending: bool = False, out=None, idx_out=N
     return kout, idx
 
 
+def radix_sort_rows(keys: torch.Tensor, descending: bool = False, out=None, idx_out=None, stream=None):
+    """Sort every row of a 2-D CUDA tensor on its own (the row-batched LSB radix
+    sort, scan_radix_sort_rows).  Returns (sorted rows, int32 column indices)."""
+    if not keys.is_cuda:
+        raise ScanError("radix_sort_rows expects a CUDA tensor (there is no CPU path)")
+    if keys.dtype not in SCAN_KEY or keys.dim() != 2:
+        raise ScanError("radix_sort_rows expects a 2-D tensor of a supported key dtype")
+    keys = keys.contiguous()
+    R, C = keys.shape
+    kout = torch.empty_like(keys) if out is None else out
+    idx = torch.empty((R, C), dtype=torch.int32, device=keys.device) if idx_out is None else idx_out
+    L = load()
+    kt = SCAN_KEY[keys.dtype]
+    ws = workspace(L.scan_radix_sort_rows_workspace_bytes(R, C, kt), keys.device, stream, kind="ops")
+    _check(L.scan_radix_sort_rows(_ptr(keys), _ptr(kout), _ptr(idx), R, C, kt, int(bool(descending)),
+                                  ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)), "scan_radix_sort_rows")
+    return kout, idx
+
+
 def weighted_sample(w: torch.Tensor, theta: float, cdf=None, stream=None) -> torch.Tensor:
     """P463 weighted sampling: scan w (fp32, our scan) and draw the index whose
     cumulative interval contains theta * sum(w) (R14).  Returns a 1-element
@@ -428,9 +451,10 @@ def top_p_sample(probs: torch.Tensor, p: float, u: torch.Tensor, stream=None, me
     method="select" (default): no full sort -- per row the candidates
     {q >= tau} are sorted in shared memory and scanned (scan_top_p_sample);
     rows that need more than 8192 candidates fall back to the sort path.
-    method="sort": the paper's pipeline -- descending row sort (torch.sort, a
-    library segmented sort), our row scan (scan_rows, P437) of the sorted
-    probabilities, our nucleus + inverse transform draw (scan_top_p_draw, R15).
+    method="sort": the paper's pipeline -- descending stable row sort (our
+    row-batched radix sort, scan_radix_sort_rows), our row scan (scan_rows,
+    P437) of the sorted probabilities, our nucleus + inverse transform draw
+    (scan_top_p_draw, R15).  No library kernel on either path.
 
     Returns (tokens int64 [rows], nucleus sizes int32 [rows])."""
     if not (probs.is_cuda and u.is_cuda) or probs.dtype != torch.float32 or u.dtype != torch.float32:
@@ -453,8 +477,8 @@ def top_p_sample(probs: torch.Tensor, p: float, u: torch.Tensor, stream=None, me
         tok[miss] = t2
         kept[miss] = k2
         return tok, kept
-    sp, order = torch.sort(probs, dim=1, descending=True, stable=True)
-    cdf = rows(sp)
+    sp, order = radix_sort_rows(probs, descending=True, stream=stream)
+    cdf = rows(sp, stream=stream)
     _check(load().scan_top_p_draw(_ptr(cdf), _ptr(order), R, C, cdf.stride(0), order.stride(0), float(p),
                                   _ptr(u), _ptr(tok), _ptr(kept), _stream_ptr(stream)),
            "scan_top_p_draw")

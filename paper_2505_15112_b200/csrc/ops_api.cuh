@@ -230,18 +230,37 @@ void split_ws_setup(SplitParams& p, void* ws, int64_t n)
 
 // LSB radix sort with 8-bit digits (radix.cuh): per pass count -> scan of the
 // digit-major counts (this library's exclusive scan) -> stable scatter.
+// Row-batched (segmented) form: cols > 0 sorts each of the n / cols rows.
+int64_t digit_tiles(int64_t n, int64_t cols)
+{
+    constexpr int64_t kRT = scan::radix::kTile;
+    if (cols > 0) return (n / cols) * ((cols + kRT - 1) / kRT);
+    return (n + kRT - 1) / kRT;
+}
+
+size_t digit_scan_ws(int64_t n, int64_t cols)
+{
+    const int64_t nt = digit_tiles(n, cols);
+    if (cols > 0) {
+        const int64_t tpr = (cols + scan::radix::kTile - 1) / scan::radix::kTile;
+        return scan_rows_workspace_bytes(SCAN_I32_I32, n / cols, scan::radix::kDigits * tpr);
+    }
+    return scan_rows_workspace_bytes(SCAN_I32_I32, scan::radix::kDigits, nt > 0 ? nt : 1);
+}
+
 template <int KT, int ES>
 int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, int descending, uint8_t* w,
-                void* tmp_keys, int32_t* tmp_idx, cudaStream_t s, const DevInfo& di)
+                void* tmp_keys, int32_t* tmp_idx, cudaStream_t s, const DevInfo& di, int64_t cols = 0)
 {
     using namespace scan::radix;
     // radix tiles (qualified: split::kTile / kThreads are also visible here)
     constexpr int64_t kRT = scan::radix::kTile;
     constexpr int kRThreads = scan::radix::kThreads;
     auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    const int64_t nt = (n + kRT - 1) / kRT;
+    const int64_t nt = digit_tiles(n, cols);
+    const int64_t tpr = cols > 0 ? (cols + kRT - 1) / kRT : 0;
     const int64_t nc = nt * kDigits;
-    const size_t scan_ws = up(scan_rows_workspace_bytes(SCAN_I32_I32, kDigits, nt));
+    const size_t scan_ws = up(digit_scan_ws(n, cols));
     uint32_t* counts = reinterpret_cast<uint32_t*>(w + scan_ws);
     uint32_t* offs = reinterpret_cast<uint32_t*>(w + scan_ws + up((size_t)nc * 4));
     uint32_t* dbase = reinterpret_cast<uint32_t*>(w + scan_ws + 2 * up((size_t)nc * 4));
@@ -276,6 +295,8 @@ int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, i
     p.n = n;
     p.ntiles = (int)nt;
     p.descending = descending != 0;
+    p.cols = cols;
+    p.tpr = (int)tpr;
     const int64_t g_count = (int64_t)di.sms * 4 < nt ? (int64_t)di.sms * 4 : nt;
     const int64_t g_scat = (int64_t)di.sms * occ < nt ? (int64_t)di.sms * occ : nt;
     const void* src_k = keys;
@@ -288,8 +309,11 @@ int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, i
         p.shift = 8 * ps;
         k_digit_count<KT, ES><<<(unsigned)g_count, kRThreads, 0, s>>>(p);
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        // per digit, the exclusive scan of its tile counts: 256 rows of ntiles (P437 row scan)
-        int st = scan_rows(counts, offs, kDigits, nt, nt, nt, SCAN_I32_I32, 1, w, scan_ws, s);
+        // per digit, the exclusive scan of its tile counts: 256 rows of ntiles (P437 row scan);
+        // segmented: per row, one exclusive scan over its [digit][tile] counts
+        int st = cols > 0 ? scan_rows(counts, offs, n / cols, kDigits * tpr, kDigits * tpr, kDigits * tpr, SCAN_I32_I32, 1,
+                                      w, scan_ws, s)
+                          : scan_rows(counts, offs, kDigits, nt, nt, nt, SCAN_I32_I32, 1, w, scan_ws, s);
         if (st != SCAN_OK) return st;
         const bool tma = aligned16(src_k) && (src_i == nullptr || aligned16(src_i)) && getenv("SCAN_SORT_NO_TMA") == nullptr;
         if (tma) {
@@ -361,13 +385,12 @@ int scan_split(const void* x, const int8_t* flags, void* z, int32_t* idx_out, in
 }
 
 // 8-bit-digit sort workspace: [scan ws of the 256*ntiles counts][counts][offs]
-size_t digit_ws_bytes(int64_t n)
+size_t digit_ws_bytes(int64_t n, int64_t cols = 0)
 {
     auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
-    const int64_t nt = (n + scan::radix::kTile - 1) / scan::radix::kTile;
+    const int64_t nt = digit_tiles(n, cols);
     const int64_t nc = nt * scan::radix::kDigits;
-    return up(scan_rows_workspace_bytes(SCAN_I32_I32, scan::radix::kDigits, nt > 0 ? nt : 1)) + 2 * up((size_t)nc * 4) +
-           up(scan::radix::kDigits * 4);
+    return up(digit_scan_ws(n, cols)) + 2 * up((size_t)nc * 4) + up(scan::radix::kDigits * 4);
 }
 
 size_t scan_radix_sort_workspace_bytes(int64_t n, int key_type)
@@ -452,6 +475,52 @@ static int radix_sort_impl(const void* keys, void* keys_out, int32_t* idx_out, i
     return SCAN_OK;
 }
 
+size_t scan_radix_sort_rows_workspace_bytes(int64_t rows, int64_t cols, int key_type)
+{
+    if (rows < 0 || cols < 0 || key_type < SCAN_KEY_U16 || key_type > SCAN_KEY_F32) return 0;
+    const size_t es = key_type <= SCAN_KEY_F16 ? 2 : 4;
+    auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const int64_t n = rows * cols;
+    return up(digit_ws_bytes(n, cols > 0 ? cols : 1)) + up((size_t)n * es) + up((size_t)n * 4);
+}
+
+int scan_radix_sort_rows(const void* keys, void* keys_out, int32_t* idx_out, int64_t rows, int64_t cols, int key_type,
+                         int descending, void* ws, size_t ws_bytes, void* stream)
+{
+    if (rows < 0 || cols < 0 || cols >= ((int64_t)1 << 31) || key_type < SCAN_KEY_U16 || key_type > SCAN_KEY_F32)
+        return SCAN_ERR_ARG;
+    if (rows == 0 || cols == 0) return SCAN_OK;
+    const int64_t n = rows * cols;
+    constexpr int64_t kRT = scan::radix::kTile;
+    if (rows * ((cols + kRT - 1) / kRT) >= ((int64_t)1 << 31) || rows * scan::radix::kDigits * ((cols + kRT - 1) / kRT) >
+                                                                        ((int64_t)1 << 40))
+        return SCAN_ERR_ARG;
+    const size_t need = scan_radix_sort_rows_workspace_bytes(rows, cols, key_type);
+    if (ws == nullptr || ((uintptr_t)ws & 255u) != 0 || ws_bytes < need) return SCAN_ERR_WORKSPACE;
+    if (keys == nullptr || keys_out == nullptr || idx_out == nullptr) return SCAN_ERR_ARG;
+    const int es = key_type <= SCAN_KEY_F16 ? 2 : 4;
+    if (overlap(keys, (size_t)n * es, keys_out, (size_t)n * es)) return SCAN_ERR_ARG;
+    DevInfo di;
+    int st = dev_info(di);
+    if (st != SCAN_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    uint8_t* w = (uint8_t*)ws;
+    const size_t head = up(digit_ws_bytes(n, cols));
+    void* tmp_keys = w + head;
+    int32_t* tmp_idx = reinterpret_cast<int32_t*>(w + head + up((size_t)n * es));
+    switch (key_type) {
+    case SCAN_KEY_U16: st = sort_digits<scan::split::KEY_U16, 2>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di, cols); break;
+    case SCAN_KEY_I16: st = sort_digits<scan::split::KEY_I16, 2>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di, cols); break;
+    case SCAN_KEY_F16: st = sort_digits<scan::split::KEY_F16, 2>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di, cols); break;
+    case SCAN_KEY_U32: st = sort_digits<scan::split::KEY_U32, 4>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di, cols); break;
+    case SCAN_KEY_I32: st = sort_digits<scan::split::KEY_I32, 4>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di, cols); break;
+    default: st = sort_digits<scan::split::KEY_F32, 4>(keys, keys_out, idx_out, n, descending, w, tmp_keys, tmp_idx, s, di, cols); break;
+    }
+    if (st == SCAN_OK) ws_mark_dirty(ws, need);
+    return st;
+}
+
 int scan_weighted_sample(const float* w, int64_t n, double theta, int64_t* index_out, float* cdf, void* ws,
                          size_t ws_bytes, void* stream)
 {
@@ -464,7 +533,7 @@ int scan_weighted_sample(const float* w, int64_t n, double theta, int64_t* index
     return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
 }
 
-int scan_top_p_draw(const float* cdf, const int64_t* order, int64_t rows, int64_t cols, int64_t cdf_row_stride,
+int scan_top_p_draw(const float* cdf, const int32_t* order, int64_t rows, int64_t cols, int64_t cdf_row_stride,
                     int64_t order_row_stride, float p, const float* u, int64_t* token_out, int32_t* kept_out,
                     void* stream)
 {

@@ -58,7 +58,43 @@ struct DigitParams {
     int ntiles;
     int shift;               // digit = (code >> shift) & 0xff
     int descending;
+    // Segmented (row-batched) sort: cols > 0 sorts every row of `cols` contiguous
+    // keys on its own.  Tiles never cross rows (tpr tiles per row, the last one
+    // ragged); counts / offs are laid out [row][digit][tile], so ONE exclusive row
+    // scan per row (scan_rows) gives every (digit, tile) its row-local start with
+    // the digit bases included; indices are column indices.
+    int64_t cols;
+    int tpr;
 };
+
+// Geometry of tile t: first element, element count, the row's first element,
+// the counts index of (digit 0, this tile) and the stride between digits.
+struct TileGeom {
+    int64_t t0, row0, c0;
+    int mt;
+    int64_t dstride;
+};
+__device__ __forceinline__ TileGeom tile_geom(const DigitParams& p, int t)
+{
+    TileGeom g;
+    if (p.cols > 0) {
+        const int64_t row = t / p.tpr, k = t - row * p.tpr;
+        g.row0 = row * p.cols;
+        g.t0 = g.row0 + k * kTile;
+        const int64_t rem = p.cols - k * kTile;
+        g.mt = rem > kTile ? kTile : (int)rem;
+        g.c0 = row * (int64_t)kDigits * p.tpr + k;
+        g.dstride = p.tpr;
+    } else {
+        g.row0 = 0;
+        g.t0 = (int64_t)t * kTile;
+        const int64_t rem = p.n - g.t0;
+        g.mt = rem > kTile ? kTile : (int)rem;
+        g.c0 = t;
+        g.dstride = p.ntiles;
+    }
+    return g;
+}
 
 template <int KT, int ES>
 __device__ __forceinline__ uint32_t load_key(const void* base, int64_t i)
@@ -97,24 +133,25 @@ __global__ void __launch_bounds__(kThreads) k_digit_count(const DigitParams p)
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
         for (int i = tid; i < kWarps * kDigits; i += kThreads) (&s_hist[0][0])[i] = 0;
         __syncthreads();
-        const int64_t t0 = (int64_t)t * kTile + warp * (kRounds * 32);
+        const TileGeom tg = tile_geom(p, t);
+        const int l0 = warp * (kRounds * 32);
         uint32_t key[kRounds];
 #pragma unroll
         for (int r = 0; r < kRounds; ++r) {
-            const int64_t e = t0 + r * 32 + lane;
-            key[r] = e < p.n ? load_key<KT, ES>(p.keys_in, e) : 0u;
+            const int li = l0 + r * 32 + lane;
+            key[r] = li < tg.mt ? load_key<KT, ES>(p.keys_in, tg.t0 + li) : 0u;
         }
 #pragma unroll
         for (int r = 0; r < kRounds; ++r) {
-            const int64_t e = t0 + r * 32 + lane;
-            if (e < p.n) atomicAdd(&s_hist[warp][digit_of<KT>(key[r], p.shift, p.descending)], 1u);
+            const int li = l0 + r * 32 + lane;
+            if (li < tg.mt) atomicAdd(&s_hist[warp][digit_of<KT>(key[r], p.shift, p.descending)], 1u);
         }
         __syncthreads();
         for (int d = tid; d < kDigits; d += kThreads) {
             uint32_t c = 0;
 #pragma unroll
             for (int w = 0; w < kWarps; ++w) c += s_hist[w][d];
-            p.counts[(int64_t)d * p.ntiles + t] = c;
+            p.counts[tg.c0 + (int64_t)d * tg.dstride] = c;
         }
         __syncthreads();
     }
@@ -139,8 +176,9 @@ __global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
     // digit bases: exclusive scan over d of the digit totals (last row-scan
     // entry + last tile count of every digit)
     if (tid < kDigits) {
+        // (segmented: the row scans already include the digit bases)
         const int64_t last = (int64_t)tid * p.ntiles + p.ntiles - 1;
-        const uint32_t tot = p.offs[last] + p.counts[last];
+        const uint32_t tot = p.cols > 0 ? 0u : p.offs[last] + p.counts[last];
         uint32_t incl = tot;
 #pragma unroll
         for (int k = 1; k < 32; k <<= 1) {
@@ -158,9 +196,10 @@ __global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
     }
     __syncthreads();
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        const int64_t t0 = (int64_t)t * kTile;
-        const int64_t rem = p.n - t0;
-        const int mt = rem > kTile ? kTile : (int)rem;
+        const TileGeom tg = tile_geom(p, t);
+        const int64_t t0 = tg.t0;
+        const int mt = tg.mt;
+        const int64_t tend = t0 + mt;
         for (int i = tid; i < kWarps * kDigits; i += kThreads) (&s_hist[0][0])[i] = 0;
         __syncthreads();
 
@@ -172,14 +211,14 @@ __global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
 #pragma unroll
         for (int r = 0; r < kRounds; ++r) {
             const int64_t e = w0 + r * 32 + lane;
-            const bool ok = e < p.n;
+            const bool ok = e < tend;
             key[r] = ok ? load_key<KT, ES>(p.keys_in, e) : 0u;
             if constexpr (IDX_IN) ix[r] = ok ? __ldg(p.idx_in + e) : 0;
         }
 #pragma unroll
         for (int r = 0; r < kRounds; ++r) {
             const int64_t e = w0 + r * 32 + lane;
-            const bool ok = e < p.n;
+            const bool ok = e < tend;
             const uint32_t d = digit_of<KT>(key[r], p.shift, p.descending);
             const uint32_t peers = digit_peers(d, ok);
             const uint32_t before = __popc(peers & lt_mask);
@@ -218,7 +257,8 @@ __global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
             for (int w = 0; w < warp; ++w) off += s_wsum[w];
             const uint32_t tdp = s_tdp[tid] + off;
             s_tdp[tid] = tdp;
-            s_gb[tid] = (int64_t)s_dbase[tid] + (int64_t)p.offs[(int64_t)tid * p.ntiles + t] - (int64_t)tdp;
+            s_gb[tid] = tg.row0 + (int64_t)s_dbase[tid] + (int64_t)p.offs[tg.c0 + (int64_t)tid * tg.dstride] -
+                        (int64_t)tdp;
         }
         __syncthreads();
 
@@ -226,14 +266,14 @@ __global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
 #pragma unroll
         for (int r = 0; r < kRounds; ++r) {
             const int64_t e = w0 + r * 32 + lane;
-            if (e < p.n) {
+            if (e < tend) {
                 const uint32_t k = ES == 2 ? (key[r] & 0xffffu) : key[r];
                 const uint32_t rk = ES == 2 ? (key[r] >> 16) : rank[ES == 2 ? 0 : r];
                 const uint32_t d = digit_of<KT>(k, p.shift, p.descending);
                 const uint32_t s = s_tdp[d] + s_hist[warp][d] + rk;
                 st_key[s] = (K)k;
                 if constexpr (IDX_IN) st_idx[s] = ix[r];
-                else st_idx[s] = (int32_t)e;
+                else st_idx[s] = (int32_t)(e - tg.row0);  // element (or, segmented, column) index
             }
         }
         __syncthreads();
@@ -289,10 +329,14 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
     int32_t* const st_idx = reinterpret_cast<int32_t*>(s_dyn + NB * C::kSlot + kTile * ES);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t full_tiles = p.n / kTile;
+    // a tile goes through the ring when it is whole and its bulk copies are 16-byte aligned
+    auto ring_tile = [&](const TileGeom& tg) {
+        return tg.mt == kTile && ((tg.t0 * ES) & 15) == 0 && (!IDX_IN || (tg.t0 & 3) == 0);
+    };
     if (tid < kDigits) {  // digit bases (as in k_digit_scatter)
+        // (segmented: the row scans already include the digit bases)
         const int64_t last = (int64_t)tid * p.ntiles + p.ntiles - 1;
-        const uint32_t tot = p.offs[last] + p.counts[last];
+        const uint32_t tot = p.cols > 0 ? 0u : p.offs[last] + p.counts[last];
         uint32_t incl = tot;
 #pragma unroll
         for (int k = 1; k < 32; k <<= 1) {
@@ -327,8 +371,9 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
             for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
                 if (wrapped) ptx::mbar_wait(&empty[s], ph ^ 1u);
                 uint8_t* dst = ring + s * C::kSlot;
-                if (t < full_tiles) {
-                    const int64_t t0 = (int64_t)t * kTile;
+                const TileGeom tg = tile_geom(p, t);
+                if (ring_tile(tg)) {
+                    const int64_t t0 = tg.t0;
                     ptx::mbar_arrive_expect_tx(&full[s], (uint32_t)C::kSlot);
                     ptx::tma_load_1d(dst, reinterpret_cast<const uint8_t*>(p.keys_in) + t0 * ES, C::kKeyB, &full[s], pol);
                     if constexpr (IDX_IN) ptx::tma_load_1d(dst + C::kKeyB, p.idx_in + t0, C::kIdxB, &full[s], pol);
@@ -350,10 +395,10 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
     int s = 0;
     uint32_t ph = 0;
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        const int64_t t0 = (int64_t)t * kTile;
-        const int64_t rem = p.n - t0;
-        const int mt = rem > kTile ? kTile : (int)rem;
-        const bool in_ring = t < full_tiles;
+        const TileGeom tg = tile_geom(p, t);
+        const int64_t t0 = tg.t0;
+        const int mt = tg.mt;
+        const bool in_ring = ring_tile(tg);
         for (int i = tid; i < kWarps * kDigits; i += kThreads) (&s_hist[0][0])[i] = 0;
         ptx::mbar_wait(&full[s], ph);
         const uint8_t* slot = ring + s * C::kSlot;
@@ -410,7 +455,8 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
             for (int w = 0; w < warp; ++w) off += s_wsum[w];
             const uint32_t tdp = s_tdp[tid] + off;
             s_tdp[tid] = tdp;
-            s_gb[tid] = (int64_t)s_dbase[tid] + (int64_t)p.offs[(int64_t)tid * p.ntiles + t] - (int64_t)tdp;
+            s_gb[tid] = tg.row0 + (int64_t)s_dbase[tid] + (int64_t)p.offs[tg.c0 + (int64_t)tid * tg.dstride] -
+                        (int64_t)tdp;
         }
         ptx::named_bar_sync(1, kThreads);
 #pragma unroll
@@ -423,7 +469,7 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
                 const uint32_t st = s_tdp[d] + s_hist[warp][d] + rk;
                 st_key[st] = (K)k;
                 if constexpr (IDX_IN) st_idx[st] = in_ring ? si[li] : p.idx_in[t0 + li];
-                else st_idx[st] = (int32_t)(t0 + li);
+                else st_idx[st] = (int32_t)(t0 + li - tg.row0);
             }
         }
         __syncwarp();

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kThreads) k_weighted_draw(const float* S, int6
 
 // Top-p nucleus + draw, one CTA per row of the inclusive scan C of the
 // descending-sorted probabilities.
-__global__ void __launch_bounds__(kThreads) k_top_p_draw(const float* C, const int64_t* order, int64_t cols,
+__global__ void __launch_bounds__(kThreads) k_top_p_draw(const float* C, const int32_t* order, int64_t cols,
                                                           int64_t c_stride, int64_t o_stride, float p, const float* u,
                                                           int64_t* token_out, int32_t* kept_out)
 {
@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kThreads) k_top_p_draw(const float* C, const i
     int64_t r = first_true(Cr, K, [t](float v) { return (double)v > t; }, s_br);
     if (r >= K) r = K - 1;
     if (threadIdx.x == 0) {
-        token_out[row] = __ldg(order + row * o_stride + r);
+        token_out[row] = (int64_t)__ldg(order + row * o_stride + r);
         if (kept_out) kept_out[row] = (int32_t)K;
     }
 }

@@ -170,6 +170,35 @@ def test_radix_sort_matches_torch_sort_stable(cuda, n):
             assert torch.equal(out, ref) and torch.equal(idx.to(torch.int64), ridx)
 
 
+@pytest.mark.parametrize("dt", [torch.float16, torch.int16, torch.int32, torch.float32])
+@pytest.mark.parametrize("desc", [False, True])
+def test_radix_sort_rows_parity(cuda, oracle, dt, desc):
+    """The row-batched sort (scan_radix_sort_rows): every row equals the
+    oracle's 1-bit-split sort of that row (keys and column indices), for rows of
+    one tile, several tiles + a ragged tile, and column counts that are not a
+    multiple of 4 (the non-ring tile path)."""
+    for R, C in ((1, 1), (5, 17), (3, 8192), (4, 8193), (7, 3 * 8192 + 5), (2, 100003), (64, 1000)):
+        k = _keys(dt, R * C, seed=R * 31 + C).reshape(R, C)
+        out, idx = cuda.radix_sort_rows(torch.from_numpy(k).cuda(), descending=desc)
+        out, idx = out.cpu().numpy(), idx.cpu().numpy()
+        bits = np.uint16 if k.itemsize == 2 else np.uint32
+        for r in range(R):
+            ro, ri = oracle.radix_sort(k[r], KEY_NP[dt][1], descending=desc)
+            assert np.array_equal(idx[r], ri), (dt, R, C, r)
+            assert np.array_equal(out[r].view(bits), ro.view(bits)), (dt, R, C, r)
+
+
+def test_radix_sort_rows_matches_torch_sort_c4(cuda, inputs_mod):
+    """C4 softmax rows (the top-p sort path's input), descending stable: equals
+    torch.sort(descending=True, stable=True) row by row (keys and indices)."""
+    R, C = 512, 131072
+    P = torch.empty((R, C), dtype=torch.float32, device="cuda")
+    inputs_mod.fill_device(inputs_mod.F32_SOFTMAX, 3, 0, R, C, P)
+    out, idx = cuda.radix_sort_rows(P, descending=True)
+    ref, ridx = torch.sort(P, dim=1, descending=True, stable=True)
+    assert torch.equal(out, ref) and torch.equal(idx.to(torch.int64), ridx)
+
+
 # ---------------------------------------------------------- sampling (P463, P299)
 def _valid_interval(S64, j, t, tol):
     """j is a valid inverse-transform draw for threshold t on the fp64 prefix
