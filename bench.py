@@ -322,7 +322,7 @@ def allreduce_max(vals, dev):
 class Run:
     """One config on this rank: inputs in HBM, the step, its timing."""
 
-    def __init__(self, cfg, rank, world, dev, offset=0):
+    def __init__(self, cfg, rank, world, dev, offset=0, exchange="nccl"):
         import torch
 
         from paper_2505_15112_b200 import dist as D
@@ -330,6 +330,7 @@ class Run:
         self.rank, self.world, self.dev = rank, world, dev
         w = self.w
         self.sharded = w["shard"] and world > 1
+        self.exchange = exchange
         self.total_elems = w["n"] * w["rows"]
         if self.sharded:
             lo, hi = D.shard_bounds(w["n"], world, rank)
@@ -358,7 +359,7 @@ class Run:
             S.exclusive(self.x, out=self.out2)
         elif self.sharded:
             fn = D.sharded_exclusive if "exclusive" in w["ops"] else D.sharded_inclusive
-            fn(self.x, out=self.out, mark=mark)
+            fn(self.x, out=self.out, mark=mark, exchange=self.exchange)
         else:
             (S.exclusive if "exclusive" in w["ops"] else S.inclusive)(self.x, out=self.out)
 
@@ -476,7 +477,7 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
-    run = Run(cfg, rank, world, dev, offset=args.offset)
+    run = Run(cfg, rank, world, dev, offset=args.offset, exchange=args.exchange)
     m = run.measure(args.steps, args.warmup, args.graph, barrier, clocks=ClockSampler(dev.index))
     roof, value, ms_per_step = m["roof"], m["value"], m["ms_per_step"]
     peak = roof["peak"]
@@ -523,7 +524,9 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         config = {
             "workload": w["name"], "n_elements": total_elems, "bytes_per_step": m["step_bytes"],
-            "parallelism": (f"shard{world} (contiguous shards, NCCL all-gather of shard totals)"
+            "parallelism": (f"shard{world} (contiguous shards, " + (
+                "device-initiated totals exchange over symmetric memory)" if args.exchange == "peer"
+                else "NCCL all-gather of shard totals)")
                             if sharded else (f"replicas x{world}" if world > 1 else "single GPU")),
             "pct_of_hbm_peak": round(100.0 * value / (peak * world), 2),
             "gelem_per_s": round(total_elems * (2 if cfg == "C1" else 1) * (world if not sharded and world > 1 else 1)
@@ -691,6 +694,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: test the multi-rank harness with ranks sharing one GPU (numbers not comparable)")
+    ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
+                    help="N > 1: shard totals by NCCL all-gather, or written by the kernels into "
+                         "symmetric memory over NVLink (device-initiated)")
     ap.add_argument("--offset", type=int, default=0,
                     help="scan x[K:] of a K-longer array (input off its 16-byte boundary; 1-D configs)")
     ap.add_argument("--no-other-configs", action="store_true",

@@ -171,6 +171,34 @@ SCAN_API int scan_shard_reduce(const void* in, int64_t n, int dtype, void* total
 SCAN_API int scan_shard_scan(const void* in, void* out, int64_t n, int dtype, int exclusive, const void* carry_in,
                              void* ws, size_t ws_bytes, void* stream);
 
+/* Device-initiated exchange of the shard totals: the NCCL all-gather and the
+ * carry kernel of the Reduce-Scan-Scan step folded into the two passes.
+ *   Slots: every rank owns a slot array of scan_peer_slots_bytes(G) bytes in
+ *   device memory that every other rank can write through a peer mapping
+ *   (CUDA IPC / P2P / symmetric memory over NVLink), zeroed once before the
+ *   first call.  Rank q's total for call `epoch` is written into EVERY rank's
+ *   array as two tagged 8-byte words (epoch << 32 | high / low 32 bits of the
+ *   int64 or fp64 total), with st.release.sys.
+ *   scan_shard_reduce_publish: scan_shard_reduce, then the total goes to every
+ *     rank's slots; peer_slots is a DEVICE array of G device pointers,
+ *     peer_slots[q] = rank q's slot array as addressed from this GPU.
+ *   scan_shard_scan_peers: scan_shard_scan whose carry_in is the sum of ranks
+ *     0..rank-1's totals (in rank order, as scan_carry_from_totals), read from
+ *     this rank's own slot array `slots` with ld.acquire.sys: the row kernel's
+ *     compute warps wait for the lower ranks while its producer already loads.
+ *   epoch: > 0, the same on every rank for one call, a new value per call
+ *     (e.g. a call counter).  Slots are a ring of 64 calls: a rank must not
+ *     run 64 or more calls ahead of the slowest rank (any collective or
+ *     barrier at least every 63 calls guarantees it).  G <= 32.
+ * Errors: SCAN_ERR_ARG for G outside 1..32, rank outside 0..G-1, epoch == 0 or
+ * NULL slot pointers; otherwise as scan_shard_reduce / scan_shard_scan.  A rank
+ * whose lower peers never publish waits forever: call both on every rank. */
+SCAN_API size_t scan_peer_slots_bytes(int G);
+SCAN_API int scan_shard_reduce_publish(const void* in, int64_t n, int dtype, void* total_out, void* const* peer_slots,
+                                       int G, int rank, uint32_t epoch, void* ws, size_t ws_bytes, void* stream);
+SCAN_API int scan_shard_scan_peers(const void* in, void* out, int64_t n, int dtype, int exclusive, const void* slots,
+                                   int G, int rank, uint32_t epoch, void* ws, size_t ws_bytes, void* stream);
+
 /* Measurement ceiling (not a scan): out[i] = widen(in[i]) for n elements --
  * exactly the HBM traffic of a scan of the same dtype with no scan arithmetic
  * (a 16-byte streaming copy).  bench.py times it in the same run as the scan

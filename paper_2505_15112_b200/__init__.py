@@ -95,6 +95,12 @@ def load() -> ctypes.CDLL:
         L.scan_shard_reduce.restype = I
         L.scan_shard_scan.argtypes = [P, P, I64, I, I, P, P, SZ, P]
         L.scan_shard_scan.restype = I
+        L.scan_peer_slots_bytes.argtypes = [I]
+        L.scan_peer_slots_bytes.restype = SZ
+        L.scan_shard_reduce_publish.argtypes = [P, I64, I, P, P, I, I, ctypes.c_uint32, P, SZ, P]
+        L.scan_shard_reduce_publish.restype = I
+        L.scan_shard_scan_peers.argtypes = [P, P, I64, I, I, P, I, I, ctypes.c_uint32, P, SZ, P]
+        L.scan_shard_scan_peers.restype = I
         # include/scan_ops.h
         L.scan_split_workspace_bytes.argtypes = [I64]
         L.scan_split_workspace_bytes.restype = SZ
@@ -330,6 +336,41 @@ def shard_scan(x: torch.Tensor, exclusive: bool = False, carry_in=None, ws: Work
     ws = ws if ws is not None else workspace(L.scan_shard_workspace_bytes(dt, n), x.device, stream)
     _check(L.scan_shard_scan(_ptr(x), _ptr(out), n, dt, int(bool(exclusive)), _ptr(carry_in),
                              ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)), "scan_shard_scan")
+    return out
+
+
+def peer_slots_bytes(G: int) -> int:
+    """Bytes of one rank's slot array for the device-initiated totals exchange."""
+    return int(load().scan_peer_slots_bytes(G))
+
+
+def shard_reduce_publish(x: torch.Tensor, peers_dev_ptr: int, G: int, rank: int, epoch: int,
+                         ws: Workspace | None = None, out=None, stream=None) -> torch.Tensor:
+    """shard_reduce + the total written straight into every rank's slot array
+    (`peers_dev_ptr`: device address of G device pointers, rank q's slots as
+    mapped on this GPU)."""
+    dt, _, cdt = _prep(x)
+    n = x.reshape(-1).numel()
+    L = load()
+    ws = ws if ws is not None else workspace(L.scan_shard_workspace_bytes(dt, n), x.device, stream)
+    out = torch.empty(1, dtype=cdt, device=x.device) if out is None else out
+    _check(L.scan_shard_reduce_publish(_ptr(x), n, dt, _ptr(out), ctypes.c_void_p(peers_dev_ptr), G, rank, epoch,
+                                       ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)),
+           "scan_shard_reduce_publish")
+    return out
+
+
+def shard_scan_peers(x: torch.Tensor, exclusive: bool, slots: torch.Tensor, G: int, rank: int, epoch: int,
+                     ws: Workspace | None = None, out=None, stream=None) -> torch.Tensor:
+    """shard_scan whose carry is read (in-kernel) from this rank's slot array."""
+    dt, odt, _ = _prep(x)
+    x = x.reshape(-1)
+    n = x.numel()
+    out = torch.empty(n, dtype=odt, device=x.device) if out is None else out
+    L = load()
+    ws = ws if ws is not None else workspace(L.scan_shard_workspace_bytes(dt, n), x.device, stream)
+    _check(L.scan_shard_scan_peers(_ptr(x), _ptr(out), n, dt, int(bool(exclusive)), _ptr(slots), G, rank, epoch,
+                                   ctypes.c_void_p(ws.ptr), ws.nbytes, _stream_ptr(stream)), "scan_shard_scan_peers")
     return out
 
 

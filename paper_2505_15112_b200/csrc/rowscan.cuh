@@ -18,6 +18,7 @@
 // cols*sizeof(In) and cols*4 multiples of 128 bytes, strides multiples of 16 B.
 #pragma once
 #include "mcscan.cuh"
+#include "shard.cuh"  // device-initiated totals exchange (wait_carry_from_slots)
 
 namespace scan {
 
@@ -36,6 +37,15 @@ struct RowParams {
     // (int64 for integer dtypes, double for floats); both NULL for plain rows.
     const void* row_pre;
     const void* carry_in;
+    // Device-initiated exchange (sharded pass 2 without NCCL): if non-NULL the
+    // carry is the sum of ranks 0..peer_rank-1's totals, read from this rank's
+    // slot array (shard.cuh) by every compute warp before its first row -- the
+    // producer's first loads overlap the wait; CTA 0 leaves it in carry_out.
+    const uint64_t* peer_slots;
+    int peer_G;
+    int peer_rank;
+    uint32_t peer_epoch;
+    void* carry_out;
 };
 
 template <int DT, int NC, int GPW, int NB>
@@ -187,6 +197,14 @@ __global__ void __launch_bounds__((2 + NC) * 32, 1) k_rowscan16(const __grid_con
         // ============ compute: one tile at a time, running row carry ============
         const int cw = warp - 2;
         Carry carry = Carry(0);
+        using Sum64 = typename std::conditional<Tr::kFloat, double, long long>::type;
+        Sum64 c_in = Sum64(0);  // carry of the lower shards (sharded pass 2)
+        if (p.peer_slots != nullptr) {
+            c_in = shard::wait_carry_from_slots<Sum64>(p.peer_slots, p.peer_G, p.peer_rank, p.peer_epoch, lane);
+            if (blockIdx.x == 0 && cw == 0 && lane == 0 && p.carry_out) *reinterpret_cast<Sum64*>(p.carry_out) = c_in;
+        } else if (p.row_pre != nullptr && p.carry_in != nullptr) {
+            c_in = *reinterpret_cast<const Sum64*>(p.carry_in);
+        }
         for (int64_t q = 0;; ++q) {
             const int s = (int)(q % NB);
             ptx::mbar_wait(&in_full[s], (uint32_t)(q / NB) & 1u);
@@ -199,13 +217,10 @@ __global__ void __launch_bounds__((2 + NC) * 32, 1) k_rowscan16(const __grid_con
             if (k == 0) {  // a new row starts from zero (P437) or from its block prefix (sharded pass 2)
                 carry = Carry(0);
                 if (p.row_pre != nullptr) {
-                    if constexpr (Tr::kFloat) {
-                        const double c0 = p.carry_in ? *reinterpret_cast<const double*>(p.carry_in) : 0.0;
-                        carry = c0 + reinterpret_cast<const double*>(p.row_pre)[row];
-                    } else {
-                        const long long c0 = p.carry_in ? *reinterpret_cast<const long long*>(p.carry_in) : 0ll;
-                        carry = (Carry)(uint32_t)(uint64_t)(c0 + reinterpret_cast<const long long*>(p.row_pre)[row]);
-                    }
+                    if constexpr (Tr::kFloat)
+                        carry = c_in + reinterpret_cast<const double*>(p.row_pre)[row];
+                    else
+                        carry = (Carry)(uint32_t)(uint64_t)(c_in + reinterpret_cast<const long long*>(p.row_pre)[row]);
                 }
             }
             const int m = (int)(p.cols - (int64_t)k * TILE < TILE ? p.cols - (int64_t)k * TILE : TILE);

@@ -542,6 +542,11 @@ struct RowVariant {
         p.exclusive = sp.exclusive;
         p.row_pre = sp.row_pre;
         p.carry_in = sp.row_pre ? sp.carry_in : nullptr;
+        p.peer_slots = sp.peer_slots;
+        p.peer_G = sp.peer_G;
+        p.peer_rank = sp.peer_rank;
+        p.peer_epoch = sp.peer_epoch;
+        p.carry_out = sp.carry_out;
         int64_t grid = di.sms;
         if (grid > sp.num_segs) grid = sp.num_segs;
         k_rowscan16<DT, NC, GPW, NB><<<(unsigned)grid, Cfg::kThreads, Cfg::kSmem, s>>>(p);

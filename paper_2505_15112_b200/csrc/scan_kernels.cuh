@@ -392,6 +392,11 @@ struct ScanParams {
     int debug;              // bit 0: skip look-back (timing only; wrong results); bit 1: spin without
                             // nanosleep; bit 2: per-CTA stall counters into the workspace
     int shift;              // MCScan SHIFT: `in` is this many elements past a 16-byte boundary
+    // rows kernel, sharded pass 2 with the device-initiated exchange (shard.cuh)
+    const uint64_t* peer_slots;
+    int peer_G, peer_rank;
+    uint32_t peer_epoch;
+    void* carry_out;
 };
 
 template <int THREADS, int ROWS>

@@ -27,13 +27,96 @@ namespace shard {
 
 constexpr int kThreads = 512;
 
+// ---- device-initiated exchange of the shard totals ----
+// Rank q's total for call `epoch` lives in every rank's slot array at entry
+// (epoch % kPeerRing) * G + q: two 8-byte words (epoch << 32 | high 32 bits of
+// the int64 / fp64 bits, epoch << 32 | low 32 bits), each one aligned 8-byte
+// store, so a reader that sees its epoch in both words has the whole value --
+// no flag, no fence order between the words.  The ring lets a rank run up to
+// kPeerRing - 1 calls ahead of the slowest reader.
+constexpr int kPeerRing = 64;
+
+struct PeerPub {
+    uint64_t* const* peers;  // device array of G pointers: rank q's slot array as seen from this GPU
+    int G;
+    int rank;
+    uint32_t epoch;
+};
+
+__device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v)
+{
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p)
+{
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void publish_total(const PeerPub& pp, uint64_t bits)
+{
+    const uint64_t tag = (uint64_t)pp.epoch << 32;
+    const int e = (int)(pp.epoch % kPeerRing) * pp.G + pp.rank;
+    for (int q = 0; q < pp.G; ++q) {
+        uint64_t* slot = pp.peers[q] + 2 * e;
+        st_release_sys_u64(slot, tag | (bits >> 32));
+        st_release_sys_u64(slot + 1, tag | (bits & 0xffffffffull));
+    }
+}
+
+// Warp-wide: wait until ranks 0..rank-1 have published call `epoch` into this
+// rank's slot array, then their totals summed in rank order (lane 0's result
+// is broadcast).  G <= 32.
+template <typename Sum>
+__device__ __forceinline__ Sum wait_carry_from_slots(const uint64_t* slots, int G, int rank, uint32_t epoch, int lane)
+{
+    uint64_t bits = 0;
+    if (lane < rank) {
+        const uint64_t* e = slots + 2 * ((int)(epoch % kPeerRing) * G + lane);
+        uint32_t backoff = 32;
+        while (true) {
+            const uint64_t hi = ld_acquire_sys_u64(e), lo = ld_acquire_sys_u64(e + 1);
+            if ((uint32_t)(hi >> 32) == epoch && (uint32_t)(lo >> 32) == epoch) {
+                bits = (hi << 32) | (lo & 0xffffffffull);
+                break;
+            }
+            __nanosleep(backoff);
+            backoff = backoff < 1024 ? backoff * 2 : 1024;
+        }
+    }
+    Sum c = Sum(0);
+    for (int q = 0; q < rank; ++q) {  // fixed order: totals[0] + ... + totals[rank-1]
+        const uint64_t b = __shfl_sync(0xffffffffu, bits, q);
+        Sum v;
+        memcpy(&v, &b, sizeof(v));
+        c += v;
+    }
+    return c;
+}
+
+// An empty shard still publishes (its total is 0).
+__global__ void k_publish_zero(PeerPub pub)
+{
+    if (threadIdx.x == 0) publish_total(pub, 0ull);
+}
+
+// One warp: the carry of a rank from its slot array (for the paths that do not
+// run the row kernel: shards shorter than a block, unaligned shards).
+template <typename Sum>
+__global__ void k_carry_from_slots(const uint64_t* slots, int G, int rank, uint32_t epoch, Sum* carry_out)
+{
+    const Sum c = wait_carry_from_slots<Sum>(slots, G, rank, epoch, threadIdx.x & 31);
+    if (threadIdx.x == 0) *carry_out = c;
+}
+
 template <int DT>
 using SumT = typename std::conditional<Traits<DT>::kFloat, double, long long>::type;
 
 template <int DT>
 __global__ void __launch_bounds__(kThreads) k_block_sums(const void* in_, int64_t n, int64_t blk, int64_t nb,
                                                          SumT<DT>* bsum, SumT<DT>* pre, void* total_out,
-                                                         uint32_t* done)
+                                                         uint32_t* done, PeerPub pub)
 {
     using Tr = Traits<DT>;
     using In = typename Tr::In;
@@ -111,6 +194,11 @@ __global__ void __launch_bounds__(kThreads) k_block_sums(const void* in_, int64_
         pre[nb] = carry;
         *reinterpret_cast<Sum*>(total_out) = carry;
         *done = 0;
+        if (pub.peers != nullptr) {  // device-initiated exchange: the total straight into every rank's slots
+            uint64_t b;
+            memcpy(&b, &carry, sizeof(b));
+            publish_total(pub, b);
+        }
     }
 }
 

@@ -99,11 +99,60 @@ def _shard_ws(x_local: torch.Tensor):
     return ws
 
 
-def _sharded(x_local: torch.Tensor, exclusive: bool, group=None, out=None, ws=None, mark=None):
+_peer_cache: dict = {}
+
+
+def _peer_state(x_local: torch.Tensor, group, world: int):
+    """This rank's slot array for the device-initiated exchange, in symmetric
+    memory (torch.distributed._symmetric_memory: every rank's buffer mapped on
+    every GPU over NVLink), with the device array of the G peer addresses."""
+    from . import ScanError, peer_slots_bytes
+    key = (x_local.device.index, id(group), world)
+    st = _peer_cache.get(key)
+    if st is None:
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+            buf = symm_mem.empty(peer_slots_bytes(world) // 8, dtype=torch.int64, device=x_local.device)
+            buf.zero_()
+            hdl = symm_mem.rendezvous(buf, group if group is not None else dist.group.WORLD)
+        except Exception as e:  # noqa: BLE001
+            raise ScanError(f"device-initiated exchange needs symmetric memory over NVLink: {e}") from e
+        torch.cuda.synchronize(x_local.device)
+        dist.barrier(group)  # every slot array zeroed before anyone publishes
+        st = _peer_cache[key] = {"buf": buf, "hdl": hdl, "peers": int(hdl.buffer_ptrs_dev), "epoch": 0}
+    return st
+
+
+def _sharded_peer(x_local, exclusive, group, out, ws, mark):
+    """Reduce-Scan-Scan with the totals exchanged by the kernels themselves:
+    pass 1 writes its total into every rank's slot array, pass 2 reads the
+    lower ranks' totals from its own (scan.h scan_shard_reduce_publish /
+    scan_shard_scan_peers) -- no NCCL call, no carry kernel."""
+    from . import shard_reduce_publish, shard_scan_peers
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    st = _peer_state(x_local, group, world)
+    st["epoch"] = st["epoch"] % 0xFFFFFFFF + 1  # the same sequence on every rank
+    ep = st["epoch"]
+    mark = mark or (lambda i: None)
+    mark(0)
+    shard_reduce_publish(x_local, st["peers"], world, rank, ep, ws=ws)
+    mark(1)
+    mark(2)  # the exchange is inside the two kernels
+    mark(3)
+    y = shard_scan_peers(x_local, exclusive, st["buf"], world, rank, ep, ws=ws, out=out)
+    mark(4)
+    return y
+
+
+def _sharded(x_local: torch.Tensor, exclusive: bool, group=None, out=None, ws=None, mark=None,
+             exchange: str = "nccl"):
     from . import carry_from_totals, shard_reduce, shard_scan
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
     ws = ws if ws is not None else _shard_ws(x_local)
+    if exchange == "peer":
+        return _sharded_peer(x_local, exclusive, group, out, ws, mark)
 
     def local_scan(x, exc, carry):
         return shard_scan(x, exc, carry_in=carry, ws=ws, out=out)
@@ -116,13 +165,16 @@ def _sharded(x_local: torch.Tensor, exclusive: bool, group=None, out=None, ws=No
     return y
 
 
-def sharded_inclusive(x_local: torch.Tensor, group=None, out=None, ws=None, mark=None) -> torch.Tensor:
+def sharded_inclusive(x_local: torch.Tensor, group=None, out=None, ws=None, mark=None,
+                      exchange: str = "nccl") -> torch.Tensor:
     """Inclusive scan of the array whose rank-r contiguous shard is x_local
     (`ws`: a reusable paper_2505_15112_b200.shard_workspace for this shard;
-    `mark`: see rss_scan)."""
-    return _sharded(x_local, False, group, out, ws, mark)
+    `mark`: see rss_scan; exchange="peer": the device-initiated totals
+    exchange over symmetric memory instead of the NCCL all-gather)."""
+    return _sharded(x_local, False, group, out, ws, mark, exchange)
 
 
-def sharded_exclusive(x_local: torch.Tensor, group=None, out=None, ws=None, mark=None) -> torch.Tensor:
+def sharded_exclusive(x_local: torch.Tensor, group=None, out=None, ws=None, mark=None,
+                      exchange: str = "nccl") -> torch.Tensor:
     """Exclusive scan of the array whose rank-r contiguous shard is x_local."""
-    return _sharded(x_local, True, group, out, ws, mark)
+    return _sharded(x_local, True, group, out, ws, mark, exchange)

@@ -110,3 +110,69 @@ def test_product_sharded_fp16_inclusive(oracle, inputs_mod):
         for y in outs:
             bad, worst, at = oracle.check_f32(y, y64[lo:hi], a64[lo:hi])
             assert bad == 0, (rank, worst, at)
+
+
+# ------------------------------------------------------------------ device-initiated exchange
+
+def _emulated_peer_exchange(cuda, x_shards, exclusive, G, epochs):
+    """G ranks emulated in ONE process on cuda:0 (B200_PROFILING.md: with fewer
+    GPUs than ranks, no rank's kernel may wait on another's concurrently): every
+    rank's pass 1 (scan_shard_reduce_publish: total -> every rank's slot array)
+    is enqueued before any pass 2 (scan_shard_scan_peers: carry from its own
+    slots), in one stream, so the in-kernel waits find their slots filled.  The
+    slot arrays are G separate device buffers and peers = their device
+    addresses, exactly what symmetric memory provides across GPUs."""
+    import torch
+    words = cuda.peer_slots_bytes(G) // 8
+    slots = [torch.zeros(words, dtype=torch.int64, device="cuda") for _ in range(G)]
+    peers = torch.tensor([s.data_ptr() for s in slots], dtype=torch.int64, device="cuda")
+    wss = [cuda.shard_workspace(x) for x in x_shards]
+    results = []
+    for ep in epochs:
+        for r in range(G):
+            cuda.shard_reduce_publish(x_shards[r], peers.data_ptr(), G, r, ep, ws=wss[r])
+        ys = [cuda.shard_scan_peers(x_shards[r], exclusive, slots[r], G, r, ep, ws=wss[r]) for r in range(G)]
+        torch.cuda.synchronize()
+        results.append([y.cpu().numpy() for y in ys])
+    return results
+
+
+@pytest.mark.parametrize("G", [1, 3, 8])
+def test_peer_exchange_emulated_int8(cuda, oracle, inputs_mod, G):
+    """Device-initiated totals exchange, int8 flags -> int32 exclusive, bit-exact
+    against the oracle over the whole array; epochs 1, 2 and 65 / 66 (the slot
+    ring of 64 wraps onto entries written by epochs 1 / 2)."""
+    import torch
+    from paper_2505_15112_b200.dist import shard_bounds
+    n = G * 3 * 131072 + 12345
+    x = inputs_mod.fill_host(inputs_mod.I8_FLAG, 2, 0, n)
+    ref = oracle.exclusive(x, "i8")
+    bounds = [shard_bounds(n, G, r) for r in range(G)]
+    shards = [torch.from_numpy(x[lo:hi]).cuda() for lo, hi in bounds]
+    for ys in _emulated_peer_exchange(cuda, shards, True, G, (1, 2, 65, 66)):
+        assert np.array_equal(np.concatenate(ys), ref)
+
+
+def test_peer_exchange_emulated_fp32_edge_shards(cuda, oracle, inputs_mod):
+    """fp32 inclusive with shards that take every pass-2 path: several blocks +
+    a tail, shorter than one block (carry by the one-warp slot reader), an empty
+    shard (publishes 0), and an unaligned shard (1-D fallback)."""
+    import torch
+    sizes = [3 * 131072 + 5, 1000, 0, 2 * 131072 + 3, 131072]
+    n = sum(sizes)
+    x = inputs_mod.fill_host(inputs_mod.F32_NORMAL, 4, 0, n + 1)
+    y64, a64, _ = oracle.inclusive(x[:n], "f32")
+    xd_all = torch.from_numpy(x).cuda()
+    shards, lo = [], 0
+    for i, m in enumerate(sizes):
+        if i == 3:  # unaligned: a copy placed one element past an aligned start
+            buf = torch.empty(m + 1, dtype=torch.float32, device="cuda")
+            buf[1:].copy_(xd_all[lo:lo + m])
+            shards.append(buf[1:])
+        else:
+            shards.append(xd_all[lo:lo + m].clone())
+        lo += m
+    for ys in _emulated_peer_exchange(cuda, shards, False, len(sizes), (7, 8)):
+        got = np.concatenate(ys)
+        bad, worst, at = oracle.check_f32(got, y64, a64)
+        assert bad == 0, (worst, at)
