@@ -178,13 +178,14 @@ SCAN_API int scan_shard_scan(const void* in, void* out, int64_t n, int dtype, in
  *   (CUDA IPC / P2P / symmetric memory over NVLink), zeroed once before the
  *   first call.  Rank q's total for call `epoch` is written into EVERY rank's
  *   array as two tagged 8-byte words (epoch << 32 | high / low 32 bits of the
- *   int64 or fp64 total), with st.release.sys.
+ *   int64 or fp64 total), relaxed system-scope stores (each word carries its
+ *   own tag, so no ordering against other memory is needed).
  *   scan_shard_reduce_publish: scan_shard_reduce, then the total goes to every
  *     rank's slots; peer_slots is a DEVICE array of G device pointers,
  *     peer_slots[q] = rank q's slot array as addressed from this GPU.
  *   scan_shard_scan_peers: scan_shard_scan whose carry_in is the sum of ranks
  *     0..rank-1's totals (in rank order, as scan_carry_from_totals), read from
- *     this rank's own slot array `slots` with ld.acquire.sys: the row kernel's
+ *     this rank's own slot array `slots` (relaxed loads until both tags match): the row kernel's
  *     compute warps wait for the lower ranks while its producer already loads.
  *   epoch: > 0, the same on every rank for one call, a new value per call
  *     (e.g. a call counter).  Slots are a ring of 64 calls: a rank must not

@@ -43,14 +43,18 @@ struct PeerPub {
     uint32_t epoch;
 };
 
-__device__ __forceinline__ void st_release_sys_u64(uint64_t* p, uint64_t v)
+// The tagged words are self-contained (the value travels inside them), so
+// neither side needs ordering against other memory: relaxed system-scope
+// accesses.  (A st.release.sys per word measured ~1.7 us each -- 28 us for
+// G = 8 -- more than the NCCL all-gather it replaces.)
+__device__ __forceinline__ void st_relaxed_sys_u64(uint64_t* p, uint64_t v)
 {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ uint64_t ld_acquire_sys_u64(const uint64_t* p)
+__device__ __forceinline__ uint64_t ld_relaxed_sys_u64(const uint64_t* p)
 {
     uint64_t v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -60,8 +64,8 @@ __device__ __forceinline__ void publish_total(const PeerPub& pp, uint64_t bits)
     const int e = (int)(pp.epoch % kPeerRing) * pp.G + pp.rank;
     for (int q = 0; q < pp.G; ++q) {
         uint64_t* slot = pp.peers[q] + 2 * e;
-        st_release_sys_u64(slot, tag | (bits >> 32));
-        st_release_sys_u64(slot + 1, tag | (bits & 0xffffffffull));
+        st_relaxed_sys_u64(slot, tag | (bits >> 32));
+        st_relaxed_sys_u64(slot + 1, tag | (bits & 0xffffffffull));
     }
 }
 
@@ -76,7 +80,7 @@ __device__ __forceinline__ Sum wait_carry_from_slots(const uint64_t* slots, int 
         const uint64_t* e = slots + 2 * ((int)(epoch % kPeerRing) * G + lane);
         uint32_t backoff = 32;
         while (true) {
-            const uint64_t hi = ld_acquire_sys_u64(e), lo = ld_acquire_sys_u64(e + 1);
+            const uint64_t hi = ld_relaxed_sys_u64(e), lo = ld_relaxed_sys_u64(e + 1);
             if ((uint32_t)(hi >> 32) == epoch && (uint32_t)(lo >> 32) == epoch) {
                 bits = (hi << 32) | (lo & 0xffffffffull);
                 break;

@@ -6,7 +6,10 @@ exclusive, n = 2^30) does, on its own shard:
   new:  scan_shard_reduce (one read) + carry_from_totals + scan_shard_scan
         (row-kernel stream with per-block starts)       [paper_2505_15112_b200.dist]
   old:  scan_total (one read) + carry_from_totals + scan with carry (MCScan)
-The NCCL all-gather of G x 8 bytes is not included (NVLink latency, ~10-20 us).
+The NCCL all-gather of G x 8 bytes is not included (NVLink latency, ~10-20 us);
+rss_peer_exchange has no all-gather at all (the totals travel inside the two
+kernels), its slot writes here are local (emulated peers) -- over NVLink each
+rank's publish adds G remote 16-byte stores.
 CUDA events, median of 5 after 2 warm-ups; rank 1's shard (nonzero carry).
 
     python profiles/shard_projection.py [C5|C3 ...]
@@ -69,8 +72,24 @@ def main():
             def single():
                 (S.exclusive if exc else S.inclusive)(x, out=y)
 
+            # device-initiated exchange: rank 1 of G, the lower rank's slot
+            # pre-published (emulated peers: all slot arrays on this GPU)
+            Gp = max(G, 2)
+            slots = [torch.zeros(S.peer_slots_bytes(Gp) // 8, dtype=torch.int64, device="cuda") for _ in range(Gp)]
+            peers = torch.tensor([t.data_ptr() for t in slots], dtype=torch.int64, device="cuda")
+            x0 = torch.zeros(1, dtype=dt, device="cuda")
+            ws0 = S.shard_workspace(x0)
+            ep = [0]
+
+            def peer():
+                ep[0] += 1
+                S.shard_reduce_publish(x0, peers.data_ptr(), Gp, 0, ep[0], ws=ws0)  # rank 0 (1 element)
+                S.shard_reduce_publish(x, peers.data_ptr(), Gp, 1, ep[0], ws=ws)
+                S.shard_scan_peers(x, exc, slots[1], Gp, 1, ep[0], ws=ws, out=y)
+
             rec = {"config": cfg, "G": G, "shard_elems": m}
-            for name, fn in (("rss_blocks", new), ("rss_mcscan", old), ("single_pass", single)):
+            for name, fn in (("rss_blocks", new), ("rss_peer_exchange", peer), ("rss_mcscan", old),
+                             ("single_pass", single)):
                 t = timed(fn)
                 rec[name] = {"per_gpu_us": round(t * 1e6, 1), "per_gpu_pct_alg": round(100 * m * bpe / t / 1e9 / peak, 1),
                              "aggregate_GBps": round(G * m * bpe / t / 1e9, 0)}
