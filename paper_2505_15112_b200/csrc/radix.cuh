@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
         const int64_t t0 = tg.t0;
         const int mt = tg.mt;
         const int64_t tend = t0 + mt;
+        const uint32_t my_off = tid < kDigits ? __ldg(p.offs + tg.c0 + (int64_t)tid * tg.dstride) : 0u;
         for (int i = tid; i < kWarps * kDigits; i += kThreads) (&s_hist[0][0])[i] = 0;
         __syncthreads();
 
@@ -257,8 +258,7 @@ __global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
             for (int w = 0; w < warp; ++w) off += s_wsum[w];
             const uint32_t tdp = s_tdp[tid] + off;
             s_tdp[tid] = tdp;
-            s_gb[tid] = tg.row0 + (int64_t)s_dbase[tid] + (int64_t)p.offs[tg.c0 + (int64_t)tid * tg.dstride] -
-                        (int64_t)tdp;
+            s_gb[tid] = tg.row0 + (int64_t)s_dbase[tid] + (int64_t)my_off - (int64_t)tdp;
         }
         __syncthreads();
 
@@ -399,6 +399,9 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
         const int64_t t0 = tg.t0;
         const int mt = tg.mt;
         const bool in_ring = ring_tile(tg);
+        // this tile's (digit, tile) starts: issued now, consumed after the rank
+        // rounds (a dependent L2 round trip per tile otherwise stalls the CTA)
+        const uint32_t my_off = tid < kDigits ? __ldg(p.offs + tg.c0 + (int64_t)tid * tg.dstride) : 0u;
         for (int i = tid; i < kWarps * kDigits; i += kThreads) (&s_hist[0][0])[i] = 0;
         ptx::mbar_wait(&full[s], ph);
         const uint8_t* slot = ring + s * C::kSlot;
@@ -407,7 +410,13 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
         ptx::named_bar_sync(1, kThreads);  // s_hist zeroed
 
         const int l0 = warp * (kRounds * 32);   // tile-local index of this warp's first element
-        uint32_t key[kRounds], rank[ES == 2 ? 1 : kRounds];
+        // 4-byte keys: the in-digit ranks wait for the CTA prefix in shared
+        // memory, each over its own element's key word in the ring slot (already
+        // in a register; the thread that read it writes it) -- 16 rank registers
+        // on top of 16 keys spilled at the 96 registers a 17-warp CTA can have.
+        // 2-byte keys pack the rank beside the key.
+        uint32_t* const s_rank = reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(slot));
+        uint32_t key[kRounds];
 #pragma unroll
         for (int r = 0; r < kRounds; ++r) {
             const int li = l0 + r * 32 + lane;
@@ -426,7 +435,7 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
             uint32_t base = 0;
             if (ok) base = s_hist[warp][d];
             if constexpr (ES == 2) key[r] |= (base + before) << 16;
-            else rank[r] = base + before;
+            else s_rank[li] = base + before;
             __syncwarp();
             if (ok && before == 0) s_hist[warp][d] = base + __popc(peers);
             __syncwarp();
@@ -455,8 +464,7 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
             for (int w = 0; w < warp; ++w) off += s_wsum[w];
             const uint32_t tdp = s_tdp[tid] + off;
             s_tdp[tid] = tdp;
-            s_gb[tid] = tg.row0 + (int64_t)s_dbase[tid] + (int64_t)p.offs[tg.c0 + (int64_t)tid * tg.dstride] -
-                        (int64_t)tdp;
+            s_gb[tid] = tg.row0 + (int64_t)s_dbase[tid] + (int64_t)my_off - (int64_t)tdp;
         }
         ptx::named_bar_sync(1, kThreads);
 #pragma unroll
@@ -464,7 +472,7 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
             const int li = l0 + r * 32 + lane;
             if (li < mt) {
                 const uint32_t k = ES == 2 ? (key[r] & 0xffffu) : key[r];
-                const uint32_t rk = ES == 2 ? (key[r] >> 16) : rank[ES == 2 ? 0 : r];
+                const uint32_t rk = ES == 2 ? (key[r] >> 16) : s_rank[li];
                 const uint32_t d = digit_of<KT>(k, p.shift, p.descending);
                 const uint32_t st = s_tdp[d] + s_hist[warp][d] + rk;
                 st_key[st] = (K)k;
