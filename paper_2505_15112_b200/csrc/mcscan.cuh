@@ -116,7 +116,8 @@ struct McParams16 {
     int debug;
     int ahead;              // reduce jobs run this many chunks ahead of scan jobs (1..4)
     int l2;                 // L2 policies: bits 0-1 Phase-I read, bits 2-3 Phase-II re-read (0 = default),
-                            // bits 4-5 after the re-read: 1 discard / 2 demote the tile's lines
+                            // bits 4-5 after the re-read: 1 discard / 2 demote the tile's lines,
+                            // bits 6-7 the output stores' policy (0 evict_first)
     int64_t seg_len;        // > 0: segmented scan of contiguous rows of seg_len >= TILE elements
                             // (carries reset at every row start); 0: one 1-D scan
     int shift;              // SHIFT instantiation: the input starts `shift` elements past a 16-byte
@@ -791,7 +792,13 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     } else if (warp == 1) {
         // =========================== storer ===========================
         if (lane == 0) {
-            const uint64_t pol = ptx::policy_evict_first();
+            // output stores: evict_first (default); p.l2 bits 6-7 = 1 evict_normal,
+            // 2 evict_unchanged, 3 evict_last (A/B of the L2 residency of the re-read)
+            const int sp_ = (p.l2 >> 6) & 3;
+            const uint64_t pol = sp_ == 1 ? ptx::policy_evict_normal()
+                                 : sp_ == 2 ? ptx::policy_evict_unchanged()
+                                 : sp_ == 3 ? ptx::policy_evict_last()
+                                            : ptx::policy_evict_first();
             Ring<NB_IN> rin;    // UNI: outputs sit in the input slots
             Ring<NSR> rout;
             uint32_t sparity = 0;  // UNI: bit s = parity of the next store_ready[s] phase (S tiles only)
