@@ -651,11 +651,43 @@ def run_e2e(args, run, dev, world, barrier):
         ms = allreduce_max([ms], dev)[0]
     h2d = x.numel() * x.element_size()
     d2h = out.numel() * out.element_size() * (2 if out2 is not None else 1)
+    # same-run ceiling: the host link moving the step's bytes both ways at once
+    # (pinned H2D and D2H of 1 GiB concurrently on two streams)
+    pcie = None
+    try:
+        nb = 1 << 30
+        hb_in = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+        hb_out = torch.empty(nb, dtype=torch.uint8, pin_memory=True)
+        da, db = torch.empty(nb, dtype=torch.uint8, device=dev), torch.empty(nb, dtype=torch.uint8, device=dev)
+        s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+        def both():
+            with torch.cuda.stream(s1):
+                da.copy_(hb_in, non_blocking=True)
+            with torch.cuda.stream(s2):
+                hb_out.copy_(db, non_blocking=True)
+        both()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            both()
+        torch.cuda.synchronize()
+        pcie = 2 * nb * 3 / (time.perf_counter() - t0) / 1e9
+        del hb_in, hb_out, da, db
+    except Exception:  # noqa: BLE001
+        pcie = None
     path = ("pinned host -> scan_host (C ABI: chunked H2D | scan | D2H on 3 streams) -> pinned host"
             if pipelined else "pinned host -> cudaMemcpyAsync -> scan (C ABI) -> cudaMemcpyAsync -> pinned host")
     step_bytes = run.total_elems * w["bpe"] * run.scans_per_step * (world if not run.sharded and world > 1 else 1)
-    return {"value": round(step_bytes / (ms / steps * 1e-3) / 1e9, 2), "unit": "GB/s",
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps, "path": path}
+    e2e_v = step_bytes / (ms / steps * 1e-3) / 1e9
+    res = {"value": round(e2e_v, 2), "unit": "GB/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": steps, "path": path}
+    if pcie:
+        # the scan's in + out bytes cross the host link once each: e2e GB/s over the
+        # link's bidirectional copy rate is the fraction of the host-link roofline
+        res["pcie_bidirectional_GBps"] = round(pcie, 1)
+        res["frac_of_pcie_bidirectional"] = round(e2e_v / pcie, 3)
+    return res
 
 
 def relaunch(args) -> int:
