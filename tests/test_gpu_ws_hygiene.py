@@ -114,3 +114,61 @@ def test_top_p_graph_replay_interleaved_with_eager(cuda, inputs_mod):
         torch.cuda.synchronize()
         assert torch.equal(tok_g, tok_ref) and torch.equal(kept_g, kept_ref)
         assert torch.equal(tok_e, tok_ref)
+
+
+def test_scans_inside_cuda_graph(cuda, oracle, inputs_mod):
+    """A 1-D MCScan (cooperative persistent launch), an unaligned one (head +
+    shifted MCScan) and a row scan captured in ONE CUDA graph and replayed
+    several times on fresh inputs: every replay bit-exact (int32)."""
+    import torch
+    n, R, C = (1 << 22) + 7, 64, 40000
+    xs = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+    Xr = torch.empty((R, C), dtype=torch.int32, device="cuda")
+    y1 = torch.empty(n, dtype=torch.int32, device="cuda")
+    y2 = torch.empty(n + 1, dtype=torch.int32, device="cuda")[1:]
+    yr = torch.empty((R, C), dtype=torch.int32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):  # warm the per-stream workspace outside the capture
+        cuda.inclusive(xs[:n], out=y1)
+        cuda.exclusive(xs[1:], out=y2)
+        cuda.rows(Xr, out=yr)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        cuda.inclusive(xs[:n], out=y1)
+        cuda.exclusive(xs[1:], out=y2)
+        cuda.rows(Xr, out=yr)
+    for it in range(3):
+        h = inputs_mod.fill_host(inputs_mod.I32_FULL, 40 + it, 0, n + 1)
+        hr = inputs_mod.fill_host(inputs_mod.I32_FULL, 50 + it, 0, R * C).reshape(R, C)
+        xs.copy_(torch.from_numpy(h))
+        Xr.copy_(torch.from_numpy(hr))
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(y1.cpu().numpy(), oracle.inclusive(h[:n], "i32")), it
+        assert np.array_equal(y2.cpu().numpy(), oracle.exclusive(h[1:], "i32")), it
+        assert np.array_equal(yr.cpu().numpy(), oracle.rows(hr, "i32")), it
+
+
+def test_new_entry_points_reject_bad_arguments(cuda):
+    """Argument checks of the round-2 C ABI calls (nothing is launched)."""
+    import torch
+    L = cuda.load()
+    x = torch.zeros(1024, dtype=torch.float32, device="cuda")
+    ws = cuda.workspace(1 << 20)
+    P = ctypes.c_void_p
+    w = P(ws.ptr)
+    # row sort: bad key type, cols >= 2^31, workspace too small
+    assert L.scan_radix_sort_rows(_p(x), _p(x), _p(x), 4, 256, 9, 0, w, ws.nbytes, _stream()) == 1
+    assert L.scan_radix_sort_rows(_p(x), _p(x), _p(x), 1, 1 << 31, 5, 0, w, ws.nbytes, _stream()) == 1
+    assert L.scan_radix_sort_rows(_p(x), _p(x), _p(x), 4, 256, 5, 0, w, 16, _stream()) == 2
+    # peer exchange: G out of range, rank >= G, epoch 0, NULL slots
+    assert L.scan_peer_slots_bytes(0) == 0 and L.scan_peer_slots_bytes(33) == 0
+    for G, r, ep, sl in ((0, 0, 1, _p(x)), (4, 4, 1, _p(x)), (4, 1, 0, _p(x)), (4, 1, 1, None)):
+        assert L.scan_shard_scan_peers(_p(x), _p(x), 1024, cuda.SCAN_F32_F32, 0, sl, G, r, ep, w, ws.nbytes,
+                                       _stream()) == 1
+        assert L.scan_shard_reduce_publish(_p(x), 1024, cuda.SCAN_F32_F32, _p(x), sl, G, r, ep, w, ws.nbytes,
+                                           _stream()) == 1
+    # top-p: workspace required
+    assert L.scan_top_p_sample(_p(x), 1, 1024, 1024, ctypes.c_float(0.9), _p(x), _p(x), None, None, 0,
+                               _stream()) == 2
