@@ -120,6 +120,8 @@ struct McParams16 {
                             // bits 6-7 the output stores' policy (0 evict_first)
     int64_t seg_len;        // > 0: segmented scan of contiguous rows of seg_len >= TILE elements
                             // (carries reset at every row start); 0: one 1-D scan
+    int wait_mode;          // mbarrier waits: bit 0 producer / storer, bit 1 compute warps sleep in the
+                            // barrier unit (suspend-time hint) instead of spinning
     int shift;              // SHIFT instantiation: the input starts `shift` elements past a 16-byte
                             // boundary; tm_in / the bulk copies address that aligned-down base
     CUtensorMap tm_in1;     // SHIFT, 2-/4-byte inputs: the same view with a one-row box (the row
@@ -759,7 +761,12 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 block_tiles(c, t0, t1);
                 const uint64_t pol = is_scan ? pol_drop : pol_keep;
                 for (int t = t0; t < t1; ++t, rin.next()) {
-                    if (rin.wrapped) ptx::mbar_wait(&in_empty[rin.s], rin.ph ^ 1u);
+                    if (rin.wrapped) {
+                        if (p.wait_mode & 1)
+                            ptx::mbar_wait_sleep(&in_empty[rin.s], rin.ph ^ 1u);
+                        else
+                            ptx::mbar_wait(&in_empty[rin.s], rin.ph ^ 1u);
+                    }
                     uint8_t* dst = in_ring + rin.s * Cfg::kRingSlot;
                     if constexpr (SZ == 1) {
                         // SHIFT: bytes from the 16-byte boundary below the tile's first
@@ -828,7 +835,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                         release(pend);
                         pend = -1;
                     }
-                    mbar_wait_prof(&store_ready[o], par, prof, &s_prof[5]);
+                    mbar_wait_prof(&store_ready[o], par, prof, &s_prof[5], (p.wait_mode & 1) != 0);
                     if (UNI) sparity ^= 1u << o;
                     if ((int64_t)t * TILE < p.n_tma_out) {
                         const int y0 = t * (TILE / 32);
@@ -969,6 +976,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         const LaneOffsets<SZ> off(e0_base);
         constexpr uint32_t GI = LaneOffsets<SZ>::kGrpIn, GO = LaneOffsets<SZ>::kGrpOut;
         const uint8_t* const gin_b = reinterpret_cast<const uint8_t*>(p.in);
+        const bool csleep = (p.wait_mode & 2) != 0;
         // L2 maintenance after the re-read (A/B, p.l2 bits 4-5); an in-place scan
         // never discards (its output lands on the same lines)
         int l2_after = (p.l2 >> 4) & 3;
@@ -1006,7 +1014,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 Carry jsum = Carry(0);
                 if constexpr (SEG) seg_r.job(t0, p.seg_len, seg_dc, gm.n);
                 for (int t = t0; t < t1; ++t, rin.next()) {
-                    mbar_wait_prof(&in_full[rin.s], rin.ph, prof0, &s_prof[1]);
+                    mbar_wait_prof(&in_full[rin.s], rin.ph, prof0, &s_prof[1], csleep);
                     const long long tr0 = prof ? clock64() : 0;
                     const uint8_t* slot = in_ring + rin.s * Cfg::kRingSlot;
                     if (SEG && t == seg_r.tile) {
@@ -1052,13 +1060,13 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 }
             } else {
                 // ---------------- Phase II: scan with the block carry ----------------
-                mbar_wait_prof(&carry_ready[c % KC], (uint32_t)(c / KC) & 1u, prof0, &s_prof[0]);
+                mbar_wait_prof(&carry_ready[c % KC], (uint32_t)(c / KC) & 1u, prof0, &s_prof[0], csleep);
                 Carry carry = s_carry[c % KC];
                 if constexpr (SEG) seg_s.job(t0, p.seg_len, seg_dc, gm.n);
                 for (int t = t0; t < t1; ++t, rin.next(), rout.next(), ++s_count) {
                     const int s = rin.s;
                     const int o = UNI ? s : rout.s;
-                    mbar_wait_prof(&in_full[s], rin.ph, prof0, &s_prof[2]);
+                    mbar_wait_prof(&in_full[s], rin.ph, prof0, &s_prof[2], csleep);
                     const long long ts0 = prof ? clock64() : 0;
                     const bool full = t < gm.full_tiles;  // warp-uniform
                     int m = TILE, m_in = TILE, m_out = TILE;
@@ -1072,7 +1080,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     }
                     if (SEG && ro > 0) {
                         // A row starts inside this tile (rare: once per row): cold path.
-                        if (!UNI && rout.wrapped) mbar_wait_prof(&out_empty[o], rout.ph ^ 1u, prof0, &s_prof[3]);
+                        if (!UNI && rout.wrapped) mbar_wait_prof(&out_empty[o], rout.ph ^ 1u, prof0, &s_prof[3], csleep);
                         const Acc agg = mc_split_tile<DT, NC, GPW, TILE>(
                             slot, out_ring + o * Cfg::kOutSlot, gin_b + (int64_t)t * TILE * SZ, gout + (int64_t)t * TILE,
                             full, m, m_in, m_out, ro, carry, exclusive, e0_base, off, &s_wt[0][0], s_count, lane, cw);
@@ -1136,7 +1144,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     const Acc wpref = __shfl_sync(0xffffffffu, lane == 0 ? Acc(0) : xe, cw);
                     const Acc agg = __shfl_sync(0xffffffffu, xi, NC - 1);
                     const long long te0 = prof ? clock64() : 0;
-                    if (!UNI && rout.wrapped) mbar_wait_prof(&out_empty[o], rout.ph ^ 1u, prof0, &s_prof[3]);
+                    if (!UNI && rout.wrapped) mbar_wait_prof(&out_empty[o], rout.ph ^ 1u, prof0, &s_prof[3], csleep);
                     uint8_t* ost = out_ring + o * Cfg::kOutSlot;
                     const long long te1 = prof ? clock64() : 0;
 #pragma unroll

@@ -95,6 +95,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
     }
 }
 
+// Blocking wait with a suspend-time hint: the warp sleeps in the barrier unit
+// until the phase completes (up to ~10 ms per try) instead of re-issuing the
+// test, so it takes no issue slots from the warps of its SM sub-partition (the
+// C2 source view counted ~50 SYNCS tests per 1,024 elements); the wake-up can
+// be later than a spinning test would notice the phase.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity)
+{
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+            : "memory");
+    } while (!ok);
+}
+
 // ---- TMA 1-D bulk copies -------------------------------------------------------
 __device__ __forceinline__ uint64_t policy_evict_first()
 {

@@ -370,6 +370,10 @@ struct Mc16Variant {
         p.debug = debug_bits();
         p.ahead = ahead < 1 ? 1 : (ahead > 4 ? 4 : ahead);
         p.l2 = env_int("SCAN_MC_L2", 0);
+        // mbarrier waits (measured, DESIGN 5.1): the producer / storer sleep in
+        // the barrier unit instead of spinning, and for 1- and 2-byte inputs (more
+        // instructions per byte) the compute warps too; SCAN_MC_WAIT overrides
+        p.wait_mode = env_int("SCAN_MC_WAIT", sizeof(In) < 4 ? 3 : 1);
         p.seg_len = segmented ? sp.seg_len : 0;
         p.gm.n = n;
         p.gm.g = di.sms < kMaxGrid ? di.sms : kMaxGrid;

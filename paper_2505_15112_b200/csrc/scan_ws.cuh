@@ -33,10 +33,13 @@ constexpr int kNumProf = 12;  // per-CTA stall counters (debug bit 2), in the pa
 
 // Timed mbarrier wait: adds the cycles spent waiting to *acc when profiling.
 __device__ __forceinline__ void mbar_wait_prof(uint64_t* bar, uint32_t parity, bool prof,
-                                               unsigned long long* acc)
+                                               unsigned long long* acc, bool sleep = false)
 {
     if (!prof) {
-        ptx::mbar_wait(bar, parity);
+        if (sleep)
+            ptx::mbar_wait_sleep(bar, parity);
+        else
+            ptx::mbar_wait(bar, parity);
         return;
     }
     if (ptx::mbar_try_wait(bar, parity)) return;
