@@ -89,10 +89,17 @@ __device__ __forceinline__ void mbar_arrive_cnt(uint64_t* bar, uint32_t count)
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity);
+
+// Blocking wait.  SCAN_WAIT_SLEEP (A/B build flag): every plain wait sleeps.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 {
+#ifdef SCAN_WAIT_SLEEP
+    mbar_wait_sleep(bar, parity);
+#else
     while (!mbar_try_wait(bar, parity)) {
     }
+#endif
 }
 
 // Blocking wait with a suspend-time hint: the warp sleeps in the barrier unit
