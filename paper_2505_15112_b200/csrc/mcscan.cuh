@@ -679,7 +679,16 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     constexpr int RS = 8;  // reduce-sum hand-off ring (ahead <= 4)
 
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* const smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-B aligned ring base.  By pointer arithmetic the compiler keeps the
+    // shared-memory provenance (LDS / STS on 32-bit addresses); through an integer
+    // round trip it loses it and emits generic LD.E / ST.E with 64-bit address
+    // math for every slot access.  Measured (DESIGN 5.1, same box, 3 runs each):
+    // shared C2 83.0 -> 86.6 %, C3 90.5 -> 91.5 %, shifted C5 -> 91.1 %, but the
+    // aligned 4-byte kernel (C5) 92.1 -> 90.4 % -- it keeps the generic form.
+    constexpr bool kGenericBase = (SZ == 4 && SH == 0);
+    uint8_t* const smem =
+        kGenericBase ? reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023)
+                     : smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr bool UNI = Cfg::kUni;
     constexpr int NSR = UNI ? NB_IN : NB_OUT;  // store_ready / out slots
     uint8_t* const in_ring = smem;
@@ -703,7 +712,19 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     const McGeom& gm = p.gm;
     const int b = blockIdx.x;
     const int njobs = gm.chunks * 2;
+    // Per-CTA stall counters (SCAN_DEBUG=4).  Their clock reads cost ~14
+    // instructions per 1,024 elements even when off, so they are compiled out of
+    // the 1- and 2-byte and shifted instantiations (C2 84.2 -> 86.6 %) unless
+    // -DSCAN_MC_PROF; the aligned 4-byte kernel keeps them: without them C5
+    // measured 92.0 -> 90.7 % (same box, 3 runs each) -- like the shared-address
+    // form below, anything that speeds up its compute warps costs C5 DRAM
+    // efficiency (DESIGN 5.1).
+    constexpr bool kProfRuntime = (sizeof(In) == 4 && SH == 0);
+#ifdef SCAN_MC_PROF
     const bool prof = (p.debug & 4) != 0;
+#else
+    const bool prof = kProfRuntime && (p.debug & 4) != 0;
+#endif
     const long long t_start = clock64();
 
     WsHeader* hdr = reinterpret_cast<WsHeader*>(p.ws);

@@ -101,6 +101,8 @@ __global__ void __launch_bounds__((2 + NC) * 32, 1) k_rowscan16(const __grid_con
     constexpr int TILE = Cfg::kTile;
 
     extern __shared__ uint8_t smem_raw[];
+    // 1024-B aligned through an integer round trip (generic slot accesses); the
+    // provenance-keeping form (LDS / STS) measured 100.5 -> 99.9 % on C4
     uint8_t* const ring = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
 
     __shared__ __align__(8) uint64_t in_full[NB];
