@@ -685,7 +685,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     // math for every slot access.  Measured (DESIGN 5.1, same box, 3 runs each):
     // shared C2 83.0 -> 86.6 %, C3 90.5 -> 91.5 %, shifted C5 -> 91.1 %, but the
     // aligned 4-byte kernel (C5) 92.1 -> 90.4 % -- it keeps the generic form.
-    constexpr bool kGenericBase = (SZ == 4 && SH == 0);
+    constexpr bool kGenericBase = (SZ == 4 && SH == 0 && !SEG);
     uint8_t* const smem =
         kGenericBase ? reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023)
                      : smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -719,7 +719,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     // measured 92.0 -> 90.7 % (same box, 3 runs each) -- like the shared-address
     // form below, anything that speeds up its compute warps costs C5 DRAM
     // efficiency (DESIGN 5.1).
-    constexpr bool kProfRuntime = (sizeof(In) == 4 && SH == 0);
+    constexpr bool kProfRuntime = (sizeof(In) == 4 && SH == 0 && !SEG);
 #ifdef SCAN_MC_PROF
     const bool prof = (p.debug & 4) != 0;
 #else
