@@ -666,13 +666,14 @@ def run_e2e(args, run, dev, world, barrier):
                 da.copy_(hb_in, non_blocking=True)
             with torch.cuda.stream(s2):
                 hb_out.copy_(db, non_blocking=True)
-        both()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(3):
+        for _ in range(2):
             both()
         torch.cuda.synchronize()
-        pcie = 2 * nb * 3 / (time.perf_counter() - t0) / 1e9
+        t0 = time.perf_counter()
+        for _ in range(5):
+            both()
+        torch.cuda.synchronize()
+        pcie = 2 * nb * 5 / (time.perf_counter() - t0) / 1e9
         del hb_in, hb_out, da, db
     except Exception:  # noqa: BLE001
         pcie = None
