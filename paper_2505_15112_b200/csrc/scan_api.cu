@@ -420,8 +420,12 @@ int launch_mc_sized(const ScanParams& p, cudaStream_t s, const DevInfo& di)
     // int8 inputs (16-KB tiles): reductions one chunk ahead with 4-tile blocks
     // (19 MB resident) -- measured 101.8 % of the copy peak on C3 against 92.6 %
     // at the 4-byte setting (ahead 2, 32 MB); DESIGN 5.1
-    const int ahead = env_int("SCAN_MC_AHEAD", sizeof(In) == 1 ? 1 : 2);
-    const int64_t resident = (int64_t)env_int("SCAN_MC_RESIDENT_MB", sizeof(In) == 1 ? 19 : 32) << 20;
+    // shifted fp16 (4 + 1 ring slots): one chunk ahead, 3-tile blocks -- 82.4 % on
+    // C2 x[1:] against 78.4 % at the default
+    const bool one_ahead = sizeof(In) == 1 || (V::SHIFT && sizeof(In) == 2);
+    const int ahead = env_int("SCAN_MC_AHEAD", one_ahead ? 1 : 2);
+    const int64_t resident =
+        (int64_t)env_int("SCAN_MC_RESIDENT_MB", sizeof(In) == 1 ? 19 : (one_ahead ? 29 : 32)) << 20;
     const int64_t per_bt = (int64_t)(ahead + 1) * di.sms * tile_bytes;
     int64_t bt = (resident + per_bt / 2) / per_bt;
     bt = bt < 2 ? 2 : bt;
