@@ -120,6 +120,9 @@ struct McParams16 {
                             // bits 6-7 the output stores' policy (0 evict_first)
     int64_t seg_len;        // > 0: segmented scan of contiguous rows of seg_len >= TILE elements
                             // (carries reset at every row start); 0: one 1-D scan
+    int bar_mode;           // chunk barrier: 0 = release-add counter per chunk, then the block sums;
+                            // 1 = block sums as epoch-tagged words polled directly (one L2 round
+                            // trip after the last publish instead of two)
     int wait_mode;          // mbarrier waits: bit 0 producer / storer, bit 1 compute warps sleep in the
                             // barrier unit (suspend-time hint) instead of spinning
     int shift;              // SHIFT instantiation: the input starts `shift` elements past a 16-byte
@@ -896,6 +899,12 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         // P248) -- whichever is ready first, so neither waits on the other.
         int next_pub = 0, next_car = 0;
         uint32_t backoff = 32;
+        // tagged mode: block sums are (call epoch << 32 | payload) words, 2 per sum for
+        // fp64 (high / low halves); the epoch is the workspace's call counter, advanced
+        // by the last CTA, so no word of an earlier call carries it
+        const bool tagged = p.bar_mode == 1;
+        constexpr int RW = Tr::kFloat ? 2 : 1;
+        const uint64_t tagw = (uint64_t)hdr->epoch << 32;
         int64_t seg_rem[SEG ? RPL : 1], seg_dc = 0;  // SEG: (start of block lane+32k of chunk next_car) mod seg_len
         if constexpr (SEG) {
             seg_dc = ((int64_t)gm.chunk_tiles * TILE) % p.seg_len;
@@ -917,24 +926,58 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 if (lane == 0) {
                     Carry t = Carry(0);
                     for (int w = 0; w < NC; ++w) t = t + s_job_sum[next_pub % RS][w];
-                    r_all[(int64_t)next_pub * gm.g + b] = carry_bits(t);
-                    ptx::red_release_add_u32(&bar[next_pub], 1u);  // orders the r store before the arrival
+                    if (tagged) {
+                        // self-contained tagged words: no fence, no counter
+                        const uint64_t bits = carry_bits(t);
+                        uint64_t* e = r_all + ((int64_t)next_pub * gm.g + b) * RW;
+                        if (RW == 2) {
+                            ptx::st_relaxed_u64(e, tagw | (bits >> 32));
+                            ptx::st_relaxed_u64(e + 1, tagw | (bits & 0xffffffffull));
+                        } else {
+                            ptx::st_relaxed_u64(e, tagw | (bits & 0xffffffffull));
+                        }
+                    } else {
+                        r_all[(int64_t)next_pub * gm.g + b] = carry_bits(t);
+                        ptx::red_release_add_u32(&bar[next_pub], 1u);  // orders the r store before the arrival
+                    }
                 }
                 __syncwarp();
                 ++next_pub;
                 progressed = true;
             }
             if (next_car < next_pub) {
-                uint32_t arrived = lane == 0 ? ld_acquire_u32(&bar[next_car]) : 0u;
-                arrived = __shfl_sync(0xffffffffu, arrived, 0);
-                if (arrived >= (uint32_t)gm.g) {
-                    const int c = next_car;
-                    uint64_t rb[RPL];
+                uint64_t rb[RPL];
+                bool ready;
+                if (tagged) {
+                    // every block sum of chunk next_car, tags checked: all present -> ready
+                    bool mine = true;
 #pragma unroll
                     for (int k = 0; k < RPL; ++k) {
                         const int bb = lane + 32 * k;
-                        rb[k] = bb < gm.g ? ld_relaxed_u64(&r_all[(int64_t)c * gm.g + bb]) : 0ull;
+                        rb[k] = 0ull;
+                        if (bb < gm.g) {
+                            const uint64_t* e = r_all + ((int64_t)next_car * gm.g + bb) * RW;
+                            const uint64_t w0 = ld_relaxed_u64(e);
+                            const uint64_t w1 = RW == 2 ? ld_relaxed_u64(e + 1) : tagw;
+                            mine = mine && (w0 >> 32) == (tagw >> 32) && (w1 >> 32) == (tagw >> 32);
+                            rb[k] = RW == 2 ? ((w0 << 32) | (w1 & 0xffffffffull)) : (w0 & 0xffffffffull);
+                        }
                     }
+                    ready = __all_sync(0xffffffffu, mine);
+                } else {
+                    uint32_t arrived = lane == 0 ? ld_acquire_u32(&bar[next_car]) : 0u;
+                    arrived = __shfl_sync(0xffffffffu, arrived, 0);
+                    ready = arrived >= (uint32_t)gm.g;
+                    if (ready) {
+#pragma unroll
+                        for (int k = 0; k < RPL; ++k) {
+                            const int bb = lane + 32 * k;
+                            rb[k] = bb < gm.g ? ld_relaxed_u64(&r_all[(int64_t)next_car * gm.g + bb]) : 0ull;
+                        }
+                    }
+                }
+                if (ready) {
+                    const int c = next_car;
                     // Segmented (rows): a block holding a row start contributes only its
                     // sum from its last row start (Phase I), and the sums before the last
                     // such block -- and the chunk carry -- do not reach later blocks.
@@ -1222,7 +1265,17 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         const uint32_t prev = ptx::claim_add(&hdr->done, 1u);
         if (prev == gridDim.x - 1) {
             // every CTA is past every barrier: reset the counters for the next call
-            for (int c = 0; c < gm.chunks; ++c) bar[c] = 0;
+            if (p.bar_mode == 1) {
+                uint32_t e = hdr->epoch + 1;
+                if (e == 0) {  // tag wrap (once per 2^32 calls): no stale word may match
+                    const int64_t nw = (int64_t)gm.chunks * gm.g * (Tr::kFloat ? 2 : 1);
+                    for (int64_t i = 0; i < nw; ++i) r_all[i] = 0ull;
+                    e = 1;
+                }
+                hdr->epoch = e;
+            } else {
+                for (int c = 0; c < gm.chunks; ++c) bar[c] = 0;
+            }
             hdr->done = 0;
             __threadfence();
         }

@@ -374,6 +374,7 @@ struct Mc16Variant {
         // the barrier unit instead of spinning, and for 1- and 2-byte inputs (more
         // instructions per byte) the compute warps too; SCAN_MC_WAIT overrides
         p.wait_mode = env_int("SCAN_MC_WAIT", sizeof(In) < 4 ? 3 : 1);
+        p.bar_mode = env_int("SCAN_MC_BAR", 0);
         p.seg_len = segmented ? sp.seg_len : 0;
         p.gm.n = n;
         p.gm.g = di.sms < kMaxGrid ? di.sms : kMaxGrid;
@@ -402,7 +403,7 @@ struct Mc16Variant {
 size_t mc_workspace_bytes(int64_t n)
 {
     const int64_t blocks = (n + 8191) / 8192 + kMaxGrid;  // r[c][b] entries, upper bound
-    return kWsDescOffset + (size_t)blocks * 8 + 64;
+    return kWsDescOffset + (size_t)blocks * 16 + 64;       // up to 2 tagged words each
 }
 
 // Chunk = G blocks of bt tiles.  Reductions run `ahead` chunks ahead of the
