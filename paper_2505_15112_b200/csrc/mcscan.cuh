@@ -120,6 +120,7 @@ struct McParams16 {
                             // bits 6-7 the output stores' policy (0 evict_first)
     int64_t seg_len;        // > 0: segmented scan of contiguous rows of seg_len >= TILE elements
                             // (carries reset at every row start); 0: one 1-D scan
+    int lazy_carry;         // Phase II waits for the block carry only at the first tile's emit
     int bar_mode;           // chunk barrier: 0 = release-add counter per chunk, then the block sums;
                             // 1 = block sums as epoch-tagged words polled directly (one L2 round
                             // trip after the last publish instead of two)
@@ -1124,8 +1125,20 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 }
             } else {
                 // ---------------- Phase II: scan with the block carry ----------------
-                mbar_wait_prof(&carry_ready[c % KC], (uint32_t)(c / KC) & 1u, prof0, &s_prof[0], csleep);
-                Carry carry = s_carry[c % KC];
+                // The carry is first needed at the first tile's emit: the tile's loads, lane
+                // prefixes and shuffle / warp-total scans run before the wait (lazy carry),
+                // hiding the chunk barrier's latency behind them.  Segmented scans take it
+                // up front (their split-tile path needs it earlier).
+                Carry carry = Carry(0);
+                bool have_carry = false;
+                auto get_carry = [&]() {
+                    if (!have_carry) {
+                        mbar_wait_prof(&carry_ready[c % KC], (uint32_t)(c / KC) & 1u, prof0, &s_prof[0], csleep);
+                        carry = s_carry[c % KC];
+                        have_carry = true;
+                    }
+                };
+                if (SEG || !(p.lazy_carry)) get_carry();
                 if constexpr (SEG) seg_s.job(t0, p.seg_len, seg_dc, gm.n);
                 for (int t = t0; t < t1; ++t, rin.next(), rout.next(), ++s_count) {
                     const int s = rin.s;
@@ -1207,6 +1220,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     const Acc xe = __shfl_up_sync(0xffffffffu, xi, 1);
                     const Acc wpref = __shfl_sync(0xffffffffu, lane == 0 ? Acc(0) : xe, cw);
                     const Acc agg = __shfl_sync(0xffffffffu, xi, NC - 1);
+                    get_carry();
                     const long long te0 = prof ? clock64() : 0;
                     if (!UNI && rout.wrapped) mbar_wait_prof(&out_empty[o], rout.ph ^ 1u, prof0, &s_prof[3], csleep);
                     uint8_t* ost = out_ring + o * Cfg::kOutSlot;

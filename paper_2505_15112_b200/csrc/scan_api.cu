@@ -375,6 +375,7 @@ struct Mc16Variant {
         // instructions per byte) the compute warps too; SCAN_MC_WAIT overrides
         p.wait_mode = env_int("SCAN_MC_WAIT", sizeof(In) < 4 ? 3 : 1);
         p.bar_mode = env_int("SCAN_MC_BAR", 0);
+        p.lazy_carry = env_int("SCAN_MC_LAZY", 0);  // A/B: measured +1.8 points at ahead 1, none at the default
         p.seg_len = segmented ? sp.seg_len : 0;
         p.gm.n = n;
         p.gm.g = di.sms < kMaxGrid ? di.sms : kMaxGrid;
