@@ -49,7 +49,7 @@
 
 namespace scan {
 
-constexpr int kMcProf = 18;
+constexpr int kMcProf = 21;  // [18..20]: coordinator publish -> complete, complete -> sums loaded, chunks
 
 // Block reductions live in the workspace after the header: r[c][b] (8 bytes
 // each, chunk-major); barrier counters in their own region (kWsBarOffset).
@@ -904,6 +904,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         // fp64 (high / low halves); the epoch is the workspace's call counter, advanced
         // by the last CTA, so no word of an earlier call carries it
         const bool tagged = p.bar_mode == 1;
+        long long t_pub[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // prof: clock at the publish of chunk c (c % 8)
         constexpr int RW = Tr::kFloat ? 2 : 1;
         const uint64_t tagw = (uint64_t)hdr->epoch << 32;
         int64_t seg_rem[SEG ? RPL : 1], seg_dc = 0;  // SEG: (start of block lane+32k of chunk next_car) mod seg_len
@@ -943,6 +944,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     }
                 }
                 __syncwarp();
+                if (prof) t_pub[next_pub & 7] = clock64();
                 ++next_pub;
                 progressed = true;
             }
@@ -969,11 +971,24 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     uint32_t arrived = lane == 0 ? ld_acquire_u32(&bar[next_car]) : 0u;
                     arrived = __shfl_sync(0xffffffffu, arrived, 0);
                     ready = arrived >= (uint32_t)gm.g;
+                    const long long t_rdy = prof ? clock64() : 0;
                     if (ready) {
 #pragma unroll
                         for (int k = 0; k < RPL; ++k) {
                             const int bb = lane + 32 * k;
                             rb[k] = bb < gm.g ? ld_relaxed_u64(&r_all[(int64_t)next_car * gm.g + bb]) : 0ull;
+                        }
+                        if (prof) {
+                            uint64_t acc = 0;
+#pragma unroll
+                            for (int k = 0; k < RPL; ++k) acc ^= rb[k];
+                            acc = __shfl_sync(0xffffffffu, acc, 0);  // the loads have landed
+                            if (lane == 0) {
+                                const long long t_val = clock64() + (long long)(acc & 0);
+                                s_prof[18] += (unsigned long long)(t_rdy - t_pub[next_car & 7]);
+                                s_prof[19] += (unsigned long long)(t_val - t_rdy);
+                                s_prof[20] += 1;
+                            }
                         }
                     }
                 }
