@@ -302,8 +302,13 @@ struct DigitTmaCfg {
     static constexpr int kSlot = kKeyB + kIdxB;
     static constexpr int kStage = kTile * (ES + 4);
     // shared memory per CTA: the first pass of 16-bit keys (no index input) may run RADIX_CTAS per SM
+#ifdef RADIX_ALL_CTAS  // A/B build: every scatter variant at RADIX_ALL_CTAS CTAs per SM
+    static constexpr bool kSmall = true;
+    static constexpr int kCtas = RADIX_ALL_CTAS;
+#else
     static constexpr bool kSmall = !IDX_IN && ES == 2;
     static constexpr int kCtas = kSmall ? RADIX_CTAS : 1;
+#endif
     static constexpr int kBudget = kSmall ? RADIX_SMEM_KB * 1024 : 200 * 1024;
     static constexpr int kNB = (kBudget - kStage) / kSlot > 4 ? 4 : (kBudget - kStage) / kSlot;
     static constexpr size_t kSmem = (size_t)kNB * kSlot + kStage;
@@ -317,7 +322,11 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
     constexpr int NB = C::kNB;
     static_assert(NB >= 2, "ring of at least two tiles");
     using K = typename std::conditional<ES == 2, uint16_t, uint32_t>::type;
+#ifdef RADIX_HIST16  // A/B build: 16-bit per-warp counts (<= kRounds * 32 per warp) -- 8 KB less
+    __shared__ uint16_t s_hist[kWarps][kDigits];
+#else
     __shared__ uint32_t s_hist[kWarps][kDigits];
+#endif
     __shared__ uint32_t s_tdp[kDigits];
     __shared__ int64_t s_gb[kDigits];
     __shared__ uint32_t s_wsum[kWarps];
