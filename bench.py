@@ -754,6 +754,10 @@ def main():
         return run_reference(args, rank)
     if world_env is None and args.gpus > 1:
         return relaunch(args)
+    import torch
+    if torch.cuda.device_count() < (local_rank + 1 if args.dist_backend == "nccl" else 1):
+        log(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, this node has {torch.cuda.device_count()}")
+        return 1
     if world != args.gpus:
         log(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
         return 2
