@@ -50,7 +50,7 @@ def test_default_line_keys_on_c1():
     assert BASE_KEYS <= set(d) and {"roofline", "gpu_launches", "clocks"} <= set(d)
     rf = d["roofline"]
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(rf) and rf["frac"] == pytest.approx(
-        rf["achieved"] / rf["peak"], rel=1e-3)
+        rf["achieved"] / rf["peak"], abs=2e-4)
     assert {"value", "unit", "cores", "kind", "sample"} <= set(d["cpu_baseline"])
     assert {"value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"} <= set(d["e2e"])
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
