@@ -146,3 +146,28 @@ def test_repeat_mcscan_500(cuda, oracle, inputs_mod, dt):
         if not torch.equal(y, (exc if e else inc)[:n]):
             bad.append((i, n, e))
     assert not bad, bad[:5]
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+@pytest.mark.parametrize("exclusive", [False, True])
+def test_unaligned_multichunk_with_carry(cuda, oracle, inputs_mod, dt, exclusive):
+    """The unaligned MCScan path (head kernel + shifted slots) with a carry-in:
+    the head starts from the carry and hands carry + head sum to the body."""
+    n = (1 << 21) + 77
+    kind = {"i32": inputs_mod.I32_FULL, "f32": inputs_mod.F32_NORMAL, "f16": inputs_mod.F16_NORMAL,
+            "i8": inputs_mod.I8_FULL}[dt]
+    out_dt = torch.int32 if dt in ("i32", "i8") else torch.float32
+    rng = np.random.default_rng(99)
+    for off_in, off_out in ((1, 0), (3, 2)):
+        h = inputs_mod.fill_host(kind, 60 + off_in, 0, n + off_in)
+        xd = _dev(h, dt)[off_in:]
+        out = torch.empty(n + off_out, dtype=out_dt, device="cuda")[off_out:]
+        if dt in ("i32", "i8"):
+            c = int(rng.integers(-(1 << 40), 1 << 40))
+            carry = torch.tensor([c], dtype=torch.int64, device="cuda")
+        else:
+            c = float(rng.normal() * 1000)
+            carry = torch.tensor([c], dtype=torch.float64, device="cuda")
+        (cuda.exclusive if exclusive else cuda.inclusive)(xd, out=out, carry_in=carry)
+        ref = (oracle.exclusive if exclusive else oracle.inclusive)(h[off_in:], dt, carry_in=c)
+        _check(oracle, out, ref, dt)
