@@ -578,8 +578,13 @@ int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t ro
     // row-ticket counter: in the caller's workspace header
     unsigned* ticket = reinterpret_cast<unsigned*>((uint8_t*)ws + scan::topp::kTicketWsOffset);
     if (cudaMemsetAsync(ticket, 0, sizeof(unsigned), (cudaStream_t)stream) != cudaSuccess) return SCAN_ERR_CUDA;
+    // SCAN_TOPP_DBG (timing A/B only, profiles/topp_phase.py): 1 stop every row after the
+    // candidate pass, 2 after the level masses, 3 after the level-L sort, 4 skip fallback
+    // rows, 5 report why a row left the level path.  SCAN_TOPP_PF: L2 bulk prefetch distance
+    // in 32-KB pass iterations, and the next row's start (measured 2-5 %, default 3)
     k_top_p<<<(unsigned)g, scan::topp::kThreads, smem, (cudaStream_t)stream>>>(probs, rows, cols, row_stride, p, u, token_out,
-                                                                    kept_out, ticket);
+                                                                    kept_out, ticket, env_int("SCAN_TOPP_DBG", 0),
+                                                                    env_int("SCAN_TOPP_PF", 3));
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
 }

@@ -132,6 +132,13 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity)
     } while (!ok);
 }
 
+// Bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, bytes a multiple of 16):
+// one instruction, no registers or shared memory held while the lines arrive.
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // ---- TMA 1-D bulk copies -------------------------------------------------------
 __device__ __forceinline__ uint64_t policy_evict_first()
 {

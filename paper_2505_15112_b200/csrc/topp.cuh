@@ -39,6 +39,7 @@ constexpr int kCap = 8192;       // candidates per row (64 KB of 64-bit keys)
 #endif
 constexpr int kLvlShift = 20;    // level = (bits(m) - bits(q)) >> 20: eighth octaves
 constexpr int kLevels = 106;     // levels of the one-pass candidate superset (13.25 octaves)
+constexpr int kLevels2 = 96;     // the third attempt's window (12 octaves) after two overflows
 constexpr int kLevCap = 2048;    // keys of one level sorted on their own
 constexpr size_t kSmemBytes = (size_t)(kCap + kLevCap) * 8;
 
@@ -259,7 +260,7 @@ constexpr size_t kTicketWsOffset = 200;  // inside the 256-byte workspace header
 
 __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64_t rows, int64_t cols, int64_t stride,
                                                     float p, const float* u, int64_t* token_out, int32_t* kept_out,
-                                                    unsigned int* ticket)
+                                                    unsigned int* ticket, int dbg, int pf)
 {
     extern __shared__ __align__(16) unsigned long long s_key[];  // kCap candidate keys, then kLevCap level keys
     unsigned long long* const s_lev = s_key + kCap;
@@ -270,7 +271,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
     __shared__ int s_level;
     __shared__ double s_lvl[kLevels];
     __shared__ unsigned s_lcnt[kLevels];
-    __shared__ unsigned long long s_wmass[kWarps][kLevels];  // per-warp fixed-point level masses
+    // per-warp fixed-point level masses as two 32-bit halves (fx >> 19, fx & (2^19 - 1)):
+    // each half of a term is < 2^19 and a level has <= 8192 terms, so both sums fit
+    // 32 bits -- native 32-bit shared atomics instead of 64-bit ones (measured: the
+    // 64-bit atomics made the level-mass step ~35 % of the kernel)
+    __shared__ unsigned s_whi[kWarps][kLevels];
+    __shared__ unsigned s_wlo[kWarps][kLevels];
     __shared__ unsigned s_wcnt[kWarps][kLevels];
     __shared__ double s_c;
     __shared__ double s_base;
@@ -280,13 +286,27 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
     const bool vec = (cols % 4 == 0) && (stride % 4 == 0) && ((reinterpret_cast<uintptr_t>(probs) & 15) == 0);
 
     __shared__ int64_t s_row;
+    // pf > 0: the CTA holds the ticket of its NEXT row too, and prefetches that row's
+    // first pf * 32 KB into L2 once the current row's pass is done (its start -- the
+    // seed loads and the first iterations -- is then an L2 hit)
+    int64_t next_row = -1;
     for (;;) {
-        if (tid == 0) s_row = (int64_t)ptx::claim_add(ticket, 1u);
+        if (tid == 0) {
+            s_row = next_row >= 0 ? next_row : (int64_t)ptx::claim_add(ticket, 1u);
+            if (pf > 0) next_row = (int64_t)ptx::claim_add(ticket, 1u);
+        }
         __syncthreads();
         const int64_t row = s_row;
         __syncthreads();
         if (row >= rows) break;
         const float* q = probs + row * stride;
+        auto prefetch_next_row = [&]() {
+            if (pf > 0 && vec && tid == 0 && next_row < rows) {
+                const int64_t n4 = cols / 4;
+                const int64_t e4 = (int64_t)pf * TOPP_UNROLL * kThreads < n4 ? (int64_t)pf * TOPP_UNROLL * kThreads : n4;
+                ptx::l2_prefetch_bulk(probs + next_row * stride, (uint32_t)(e4 * 16));
+            }
+        };
         // 1-2 (fast path, one HBM read of the row): the row maximum and, in the same
         // pass, a candidate SUPERSET -- every q whose bits are within 53 * 2^21 of the
         // running block maximum's (about q >= rmax * 2^-13.25; the running maximum only
@@ -305,15 +325,26 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
             float lm = 0.f;
             for (int64_t i = tid; i < cols && i < 4 * kThreads; i += kThreads) lm = fmaxf(lm, __ldg(q + i));
             const float m0 = block_max(lm, s_red);
+            bool over = false;
+            // attempt 0 collects relative to the running maximum; a superset overflow
+            // (the early, low running maximum admits too much) repeats the same pipelined
+            // pass with the threshold fixed at the final maximum's window (attempt 1), then
+            // with a 12-octave window (attempt 2: levels >= kLevels2 stay empty, so a
+            // nucleus reaching past them is a short mass and takes the fallback) -- one or
+            // two more row reads instead of the tau-stepping fallback and the host-side sort
+            // path (2.7 % of the C4 rows overflowed and took ~45 % of the kernel time)
+            uint32_t span = kSpan;
+            for (int attempt = 0; attempt < 3; ++attempt) {
+            span = attempt < 2 ? kSpan : ((uint32_t)kLevels2 << kLvlShift);
             if (tid == 0) {
                 s_cnt = 0;
-                s_rmax = __float_as_uint(m0);
+                s_rmax = __float_as_uint(attempt == 0 ? m0 : m);
             }
             __syncthreads();
-            bool over = false;
+            over = false;
             auto collect4 = [&](int64_t i0, const float (&v)[4], int nv) {
                 const uint32_t rb = *reinterpret_cast<volatile unsigned*>(&s_rmax);
-                const uint32_t thr = rb > kSpan ? rb - kSpan : 1u;  // bits of the collection threshold (> 0)
+                const uint32_t thr = rb > span ? rb - span : 1u;  // bits of the collection threshold (> 0)
                 uint32_t tk = 0;
                 float vm = 0.f;
 #pragma unroll
@@ -355,6 +386,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
                 // candidate) one warp compaction per 128 * TOPP_UNROLL elements of the warp
                 constexpr int kUnroll = TOPP_UNROLL;
                 const int64_t n4 = cols / 4;
+                // L2 bulk prefetch `pf` iterations (of kUnroll * kThreads float4) ahead of
+                // the loads: more bytes in flight than the registers hold
+                constexpr int64_t kIt4 = (int64_t)kUnroll * kThreads;
+                auto prefetch_it = [&](int64_t it) {
+                    const int64_t a4 = it * kIt4;
+                    if (a4 < n4) {
+                        const int64_t e4 = a4 + kIt4 < n4 ? a4 + kIt4 : n4;
+                        ptx::l2_prefetch_bulk(reinterpret_cast<const float4*>(q) + a4, (uint32_t)((e4 - a4) * 16));
+                    }
+                };
+                if (tid == 0)
+                    for (int k = 1; k <= pf; ++k) prefetch_it(k);
                 // software-pipelined: the next iteration's loads are issued before this
                 // iteration's values are screened
                 float4 nf[kUnroll];
@@ -364,6 +407,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
                     nf[r] = i4 < n4 ? __ldcs(reinterpret_cast<const float4*>(q) + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
                 }
                 for (int64_t base4 = 0; base4 < n4; base4 += kUnroll * kThreads) {
+                    if (pf > 0 && tid == 0) prefetch_it(base4 / kIt4 + 1 + pf);
                     float4 f[kUnroll];
 #pragma unroll
                     for (int r = 0; r < kUnroll; ++r) {
@@ -372,7 +416,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
                         nf[r] = i4 < n4 ? __ldcs(reinterpret_cast<const float4*>(q) + i4) : make_float4(0.f, 0.f, 0.f, 0.f);
                     }
                     const int rb = (int)*reinterpret_cast<volatile unsigned*>(&s_rmax);
-                    const int thr = rb > (int)kSpan ? rb - (int)kSpan : 1;  // bits of the threshold (> 0)
+                    const int thr = rb > (int)span ? rb - (int)span : 1;  // bits of the threshold (> 0)
                     float vm = 0.f;
                     uint32_t tk = 0;
 #pragma unroll
@@ -430,6 +474,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
             m = block_max(lm, s_red);
             over = __syncthreads_or(over);
             count = (int)s_cnt;
+            if (attempt == 0) prefetch_next_row();
+            if (!over) break;
+            }  // attempt
+            if (dbg == 1) {  // timing A/B: the pass alone
+                if (tid == 0) token_out[row] = count;
+                __syncthreads();
+                continue;
+            }
             if (!over && (__float_as_uint(m) >> 23) >= 15u) {  // fixed-point levels need E_m - 14 >= 1
                 const uint32_t mb = __float_as_uint(m);
                 // level masses in fixed point: q = mant * 2^(E_q - 150) with E_q >= E_m - 14
@@ -438,18 +490,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
                 // atomics), then one exact conversion per level
                 const int Em = (int)(mb >> 23);
                 for (int i = tid; i < kWarps * kLevels; i += kThreads) {
-                    (&s_wmass[0][0])[i] = 0ull;
+                    (&s_whi[0][0])[i] = 0u;
+                    (&s_wlo[0][0])[i] = 0u;
                     (&s_wcnt[0][0])[i] = 0u;
                 }
                 __syncthreads();
                 for (int i = tid; i < count; i += kThreads) {
                     const uint32_t code = (uint32_t)(s_key[i] >> 32) & 0x7fffffffu;
                     const uint32_t d = mb - code;  // code <= mb
-                    if (d < kSpan) {
+                    if (d < span) {
                         const int Eq = (int)(code >> 23);
                         const unsigned long long fx = (unsigned long long)((code & 0x7fffffu) | 0x800000u)
                                                       << (Eq - Em + 14);
-                        atomicAdd(&s_wmass[warp][d >> kLvlShift], fx);
+                        atomicAdd(&s_whi[warp][d >> kLvlShift], (unsigned)(fx >> 19));
+                        atomicAdd(&s_wlo[warp][d >> kLvlShift], (unsigned)fx & 0x7ffffu);
                         atomicAdd(&s_wcnt[warp][d >> kLvlShift], 1u);
                     }
                 }
@@ -458,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
                     unsigned long long sm = 0ull;
                     unsigned c = 0u;
                     for (int w = 0; w < kWarps; ++w) {
-                        sm += s_wmass[w][l];
+                        sm += ((unsigned long long)s_whi[w][l] << 19) + s_wlo[w][l];
                         c += s_wcnt[w][l];
                     }
                     s_lvl[l] = ldexp((double)sm, Em - 164);
@@ -469,6 +523,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
                 if (warp == 0) warp_first_level<false>(s_lvl, s_lcnt, kLevels, (double)p, &s_level, &s_base, &s_aux[0]);
                 __syncthreads();
                 const int L = s_level;
+                if (dbg == 2) {  // timing A/B: pass + level masses + level search
+                    if (tid == 0) token_out[row] = L >= 0 ? (int64_t)s_lcnt[L] : -2;
+                    __syncthreads();
+                    continue;
+                }
                 if (L >= 0 && s_lcnt[L] <= (unsigned)kLevCap) {
                     // ---- level path: sort level L only (and the draw's level) ----
                     const int nL = block_extract_level(s_key, count, mb, L, s_lev, kLevCap, &s_cnt);
@@ -477,6 +536,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
                     if (nL <= kLevCap / 2) block_rank_sort_desc(s_lev, nL, s_lev + kLevCap / 2);
                     else block_sort_desc(s_lev, nL);
                     const int jL = block_first_crossing<false>(s_lev, nL, baseL, (double)p, s_dred, &s_min, &s_c);
+                    if (dbg == 3) {  // timing A/B: ... + level L sorted, K found
+                        if (tid == 0) token_out[row] = nL;
+                        __syncthreads();
+                        continue;
+                    }
                     if (jL < nL) {  // always: cum(<= L) >= p
                         const int K = nbefL + jL + 1;
                         const double CK = s_c;
@@ -549,6 +613,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
             }
         }
 
+        if (dbg == 5) {  // diagnostics: rows the level path did not finish, by cause (-10 - code)
+            if (tid == 0) token_out[row] = -10 - (ok ? (count > kLevCap ? 3 : 0) : (count > kCap ? 1 : 2));
+            __syncthreads();
+            continue;
+        }
+        if (dbg == 4 && !ok) {  // timing A/B: rows that need the fallback are skipped
+            if (tid == 0) token_out[row] = 0;
+            __syncthreads();
+            continue;
+        }
         // 1-2 (fallback): candidates {q >= tau} until their mass reaches p
         for (int sh = 8; !ok && sh <= 160; sh += 4) {
             const float tau = sh >= 150 ? 0.f : ldexpf(m, -sh);
