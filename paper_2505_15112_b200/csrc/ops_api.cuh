@@ -575,6 +575,9 @@ int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t ro
     if (err != cudaSuccess) return SCAN_ERR_CUDA;
     const int per_sm = env_int("SCAN_TOPP_CTAS_PER_SM", occ) < occ ? env_int("SCAN_TOPP_CTAS_PER_SM", occ) : occ;
     const int64_t g = (int64_t)di.sms * per_sm < rows ? (int64_t)di.sms * per_sm : rows;
+    // the first pass's candidate window in eighth-octave levels (SCAN_TOPP_W0, 8..106)
+    int w0 = env_int("SCAN_TOPP_W0", 98);
+    w0 = w0 < 8 ? 8 : (w0 > scan::topp::kLevels ? scan::topp::kLevels : w0);
     // row-ticket counter: in the caller's workspace header
     unsigned* ticket = reinterpret_cast<unsigned*>((uint8_t*)ws + scan::topp::kTicketWsOffset);
     if (cudaMemsetAsync(ticket, 0, sizeof(unsigned), (cudaStream_t)stream) != cudaSuccess) return SCAN_ERR_CUDA;
@@ -584,7 +587,8 @@ int scan_top_p_sample(const float* probs, int64_t rows, int64_t cols, int64_t ro
     // in 32-KB pass iterations, and the next row's start (measured 2-5 %, default 3)
     k_top_p<<<(unsigned)g, scan::topp::kThreads, smem, (cudaStream_t)stream>>>(probs, rows, cols, row_stride, p, u, token_out,
                                                                     kept_out, ticket, env_int("SCAN_TOPP_DBG", 0),
-                                                                    env_int("SCAN_TOPP_PF", 3));
+                                                                    env_int("SCAN_TOPP_PF", 3),
+                                                                    w0);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
 }

@@ -260,7 +260,7 @@ constexpr size_t kTicketWsOffset = 200;  // inside the 256-byte workspace header
 
 __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64_t rows, int64_t cols, int64_t stride,
                                                     float p, const float* u, int64_t* token_out, int32_t* kept_out,
-                                                    unsigned int* ticket, int dbg, int pf)
+                                                    unsigned int* ticket, int dbg, int pf, int w0)
 {
     extern __shared__ __align__(16) unsigned long long s_key[];  // kCap candidate keys, then kLevCap level keys
     unsigned long long* const s_lev = s_key + kCap;
@@ -290,11 +290,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
     // first pf * 32 KB into L2 once the current row's pass is done (its start -- the
     // seed loads and the first iterations -- is then an L2 hit)
     int64_t next_row = -1;
+    // a row whose nucleus reached past attempt 0's narrower window is redone from
+    // attempt 1 (uniform: every thread sets it from shared state)
+    int64_t redo = -1;
     for (;;) {
+        const int first_attempt = redo >= 0 ? 1 : 0;
         if (tid == 0) {
-            s_row = next_row >= 0 ? next_row : (int64_t)ptx::claim_add(ticket, 1u);
-            if (pf > 0) next_row = (int64_t)ptx::claim_add(ticket, 1u);
+            if (redo >= 0) {
+                s_row = redo;
+            } else {
+                s_row = next_row >= 0 ? next_row : (int64_t)ptx::claim_add(ticket, 1u);
+                if (pf > 0) next_row = (int64_t)ptx::claim_add(ticket, 1u);
+            }
         }
+        redo = -1;
         __syncthreads();
         const int64_t row = s_row;
         __syncthreads();
@@ -318,6 +327,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
         int count = 0;
         bool ok = false;
         float m = 0.f;
+        int used_attempt = 0;
         {
             constexpr uint32_t kSpan = (uint32_t)kLevels << kLvlShift;
             // seed the running maximum with the first 4 * kThreads elements' maximum
@@ -334,8 +344,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
             // two more row reads instead of the tau-stepping fallback and the host-side sort
             // path (2.7 % of the C4 rows overflowed and took ~45 % of the kernel time)
             uint32_t span = kSpan;
-            for (int attempt = 0; attempt < 3; ++attempt) {
-            span = attempt < 2 ? kSpan : ((uint32_t)kLevels2 << kLvlShift);
+            for (int attempt = first_attempt; attempt < 3; ++attempt) {
+            // attempt 0's window (w0 levels, default 12.25 octaves) is narrower than the
+            // fixed-threshold retry's: ~30 % fewer candidates (their extraction was ~40 % of
+            // the pass's instructions); a nucleus reaching past it redoes the row
+            span = attempt == 0 ? ((uint32_t)w0 << kLvlShift)
+                                : (attempt == 1 ? kSpan : ((uint32_t)kLevels2 << kLvlShift));
+            used_attempt = attempt;
             if (tid == 0) {
                 s_cnt = 0;
                 s_rmax = __float_as_uint(attempt == 0 ? m0 : m);
@@ -523,6 +538,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
                 if (warp == 0) warp_first_level<false>(s_lvl, s_lcnt, kLevels, (double)p, &s_level, &s_base, &s_aux[0]);
                 __syncthreads();
                 const int L = s_level;
+                if (L < 0 && used_attempt == 0 && w0 < kLevels) {  // short mass in the narrow window
+                    redo = row;
+                    __syncthreads();
+                    continue;
+                }
                 if (dbg == 2) {  // timing A/B: pass + level masses + level search
                     if (tid == 0) token_out[row] = L >= 0 ? (int64_t)s_lcnt[L] : -2;
                     __syncthreads();
