@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
     // a row whose nucleus reached past attempt 0's narrower window is redone from
     // attempt 1 (uniform: every thread sets it from shared state)
     int64_t redo = -1;
+    float redo_m = 0.f;  // the redone row's maximum (attempt 1's threshold)
     for (;;) {
         const int first_attempt = redo >= 0 ? 1 : 0;
         if (tid == 0) {
@@ -326,7 +327,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
         // and the candidates {l <= L} -- an upward-closed set holding the nucleus.
         int count = 0;
         bool ok = false;
-        float m = 0.f;
+        float m = first_attempt == 1 ? redo_m : 0.f;
         int used_attempt = 0;
         {
             constexpr uint32_t kSpan = (uint32_t)kLevels << kLvlShift;
@@ -540,6 +541,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_top_p(const float* probs, int64
                 const int L = s_level;
                 if (L < 0 && used_attempt == 0 && w0 < kLevels) {  // short mass in the narrow window
                     redo = row;
+                    redo_m = m;
                     __syncthreads();
                     continue;
                 }
