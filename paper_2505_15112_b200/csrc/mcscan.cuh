@@ -119,6 +119,7 @@ struct McJob {
 __device__ __forceinline__ int mc_njobs(int chunks, int bt, int jgrp, int ilv)
 {
     if (ilv > 0) return ilv + 2 * chunks * bt;
+    if (ilv < 0) return (-ilv + 1) / 2 + 3 * chunks;  // two-tile interleave (bt = 2, odd D = -ilv)
     return 2 * jgrp * ((chunks + jgrp - 1) / jgrp);
 }
 // c >= chunks: no job at this position (skip it)
@@ -130,6 +131,39 @@ __device__ __forceinline__ McJob mc_job_x(int q, int chunks, int bt, int ahead, 
         J.j0 = 0;
         J.j1 = bt;
         J.first = J.last = true;
+        return J;
+    }
+    if (ilv < 0) {
+        // two-tile interleave, bt = 2, odd D: steps m = 0, 1, ... reduce tiles
+        // 2m + D (the second tile of its chunk) and 2m + D + 1 (the first of the
+        // next) and scan tiles 2m, 2m + 1 (one chunk) -- two-tile R / S runs like
+        // the default schedule, with the reduce D tiles ahead of the scan.  The
+        // prologue reduces tiles 0 .. D - 1 ((D - 1) / 2 whole chunks + one tile).
+        const int D = -ilv;
+        const int P = (D + 1) / 2;
+        int k0, n;
+        if (q < P) {
+            J.is_scan = false;
+            k0 = 2 * q;
+            n = (q < P - 1) ? 2 : 1;
+        } else {
+            const int qq = q - P, m = qq / 3, r = qq - 3 * m;
+            J.is_scan = r == 2;
+            k0 = r == 2 ? 2 * m : 2 * m + D + r;
+            n = r == 2 ? 2 : 1;
+        }
+        J.c = k0 >> 1;
+        if (J.c >= chunks) {
+            J.c = chunks;
+            J.is_scan = false;
+            J.j0 = J.j1 = 0;
+            J.first = J.last = false;
+            return J;
+        }
+        J.j0 = k0 & 1;
+        J.j1 = J.j0 + n;
+        J.first = J.j0 == 0;
+        J.last = J.j1 == 2;
         return J;
     }
     const int K = chunks * bt;

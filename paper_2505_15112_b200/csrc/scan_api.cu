@@ -380,6 +380,8 @@ struct Mc16Variant {
         if (p.jgrp < 1) p.jgrp = 1;
         while (p.jgrp > 1 && p.jgrp * (p.ahead + 1) > 8) --p.jgrp;  // carry / block-sum rings hold 8 chunks
         p.ilv = env_int("SCAN_MC_ILV", 0);  // tile-interleaved schedule (A/B), D tiles ahead
+        // two-tile interleave (A/B, SCAN_MC_ILV2 = odd D): needs bt = 2 (checked below)
+        if (env_int("SCAN_MC_ILV2", 0) > 0) p.ilv = -(env_int("SCAN_MC_ILV2", 0) | 1);
         p.seg_len = segmented ? sp.seg_len : 0;
         p.gm.n = n;
         p.gm.g = di.sms < kMaxGrid ? di.sms : kMaxGrid;
@@ -393,6 +395,7 @@ struct Mc16Variant {
         if ((ntiles + (int64_t)p.gm.g * bt64 - 1) / ((int64_t)p.gm.g * bt64) > kMaxChunks)  // counters must fit
             bt64 = (ntiles + (int64_t)kMaxChunks * p.gm.g - 1) / ((int64_t)kMaxChunks * p.gm.g);
         p.gm.bt = (int)bt64;
+        if (p.ilv < 0 && p.gm.bt != 2) p.ilv = 0;  // the two-tile interleave is defined for bt = 2
         p.gm.chunk_tiles = p.gm.g * p.gm.bt;
         p.gm.chunks = (int)((ntiles + p.gm.chunk_tiles - 1) / p.gm.chunk_tiles);
         void* args[] = {&p};

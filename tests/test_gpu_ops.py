@@ -299,6 +299,44 @@ def test_top_p_select_edge_rows(cuda, oracle):
                 assert int(tok[r]) == rt and int(kept[r]) == rk, (p, r, int(tok[r]), rt, int(kept[r]), rk)
 
 
+def test_top_p_select_retry_paths(cuda, oracle, inputs_mod, monkeypatch):
+    """The select kernel's retries: (a) a row whose running-maximum superset
+    overflows (the early maximum is tiny) but whose final-maximum window fits;
+    (b) a row whose nucleus reaches 12.6 octaves below the maximum, past the
+    first attempt's 12.25-octave window (redone from the fixed-threshold
+    attempt); (c) C4 rows with a 5-octave first window, so most rows are redone.
+    Every token and nucleus size is the oracle's."""
+    C = 131072
+    rng = np.random.default_rng(11)
+    M = np.float32(0.01)
+    ra = np.zeros(C, np.float32)
+    ra[:2048] = 1e-12                                                        # tiny early maximum
+    ra[2048:22048] = M * np.float32(2.0 ** -15)                               # below the final window
+    hot = rng.choice(np.arange(30000, C), 3000, replace=False)
+    ra[hot] = M * (0.5 + 0.5 * rng.random(3000)).astype(np.float32)
+    rb = np.zeros(C, np.float32)
+    rb[77] = M
+    far = rng.choice(np.arange(1000, C), 5000, replace=False)
+    rb[far] = M * np.float32(2.0 ** -12.6)                                    # 12.6 octaves down
+    P = np.stack([ra, rb])
+    u = np.array([0.35, 0.8], np.float32)
+    for p in (0.5, 0.9, 0.99):
+        tok, kept = cuda.top_p_sample(torch.from_numpy(P).cuda(), p, torch.from_numpy(u).cuda())
+        for r in range(2):
+            rt, rk = oracle.top_p_sample(P[r], float(np.float32(p)), float(u[r]))
+            assert int(tok[r]) == rt and int(kept[r]) == rk, (p, r, int(tok[r]), rt, int(kept[r]), rk)
+    # (c) forced redo of most C4 rows (the window knob is read at every launch)
+    R = 16
+    Pc = inputs_mod.fill_host(inputs_mod.F32_SOFTMAX, 3, 0, R, C)
+    uc = rng.random(R).astype(np.float32)
+    monkeypatch.setenv("SCAN_TOPP_W0", "40")
+    tok, kept = cuda.top_p_sample(torch.from_numpy(Pc).cuda(), 0.9, torch.from_numpy(uc).cuda())
+    monkeypatch.delenv("SCAN_TOPP_W0")
+    for r in range(R):
+        rt, rk = oracle.top_p_sample(Pc[r], float(np.float32(0.9)), float(uc[r]))
+        assert int(tok[r]) == rt and int(kept[r]) == rk, (r, int(tok[r]), rt, int(kept[r]), rk)
+
+
 @pytest.mark.slow
 def test_top_p_full_c4(cuda, oracle, inputs_mod):
     """bench_ops' top-p workload (4096 C4 rows, p = 0.9): the sort-free path and
