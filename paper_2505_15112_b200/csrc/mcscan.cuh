@@ -49,8 +49,7 @@
 
 namespace scan {
 
-constexpr int kMcProf = 24;  // [18..20]: coordinator publish -> complete, complete -> sums loaded, chunks;
-                             // [21..23]: compute warp 0 in R jobs, in S jobs (waits included), whole job loop
+constexpr int kMcProf = 21;  // [18..20]: coordinator publish -> complete, complete -> sums loaded, chunks
 
 // Block reductions live in the workspace after the header: r[c][b] (8 bytes
 // each, chunk-major); barrier counters in their own region (kWsBarOffset).
@@ -85,111 +84,6 @@ __device__ __forceinline__ void mc_job(int q, int chunks, int ahead, int& c, boo
         c = P + (qq - 2 * P);
         is_scan = true;
     }
-}
-
-// Jobs in groups of `grp` chunks: the R / S order of mc_job over super-chunks
-// of grp consecutive chunks (grp = 1: mc_job).  Chunks past the end (the last
-// super-chunk may be partial) come out as c >= chunks and are skipped.
-__device__ __forceinline__ void mc_job_g(int q, int chunks, int ahead, int grp, int& c, bool& is_scan)
-{
-    if (grp <= 1) {
-        mc_job(q, chunks, ahead, c, is_scan);
-        return;
-    }
-    const int sc_n = (chunks + grp - 1) / grp;
-    int sc;
-    mc_job(q / grp, sc_n, ahead, sc, is_scan);
-    c = sc * grp + q % grp;
-}
-
-// One job of a CTA's sequence: chunk c, R (reduce) or S (scan), tiles [j0, j1)
-// of the CTA's block in that chunk; `first` / `last`: the job starts / ends the
-// block (S takes the block carry at its first tile, R publishes the block sum
-// after its last).  ilv = 0: whole-block jobs in the mc_job_g order.  ilv = D >
-// 0: tile-interleaved -- the CTA's tiles k = 0, 1, ... (chunk k / bt, tile k % bt)
-// run as r_0 .. r_{D-1}, then (r_{k+D}, s_k) pairs: the reduce of a tile runs D
-// tiles ahead of its scan, so the resident input is D + 1 tiles per CTA while
-// a chunk's barrier has D - bt + 1 (r, s) pairs to complete.
-struct McJob {
-    int c;
-    bool is_scan;
-    int j0, j1;
-    bool first, last;
-};
-__device__ __forceinline__ int mc_njobs(int chunks, int bt, int jgrp, int ilv)
-{
-    if (ilv > 0) return ilv + 2 * chunks * bt;
-    if (ilv < 0) return (-ilv + 1) / 2 + 3 * chunks;  // two-tile interleave (bt = 2, odd D = -ilv)
-    return 2 * jgrp * ((chunks + jgrp - 1) / jgrp);
-}
-// c >= chunks: no job at this position (skip it)
-__device__ __forceinline__ McJob mc_job_x(int q, int chunks, int bt, int ahead, int jgrp, int ilv)
-{
-    McJob J;
-    if (ilv <= 0) {
-        mc_job_g(q, chunks, ahead, jgrp, J.c, J.is_scan);
-        J.j0 = 0;
-        J.j1 = bt;
-        J.first = J.last = true;
-        return J;
-    }
-    if (ilv < 0) {
-        // two-tile interleave, bt = 2, odd D: steps m = 0, 1, ... reduce tiles
-        // 2m + D (the second tile of its chunk) and 2m + D + 1 (the first of the
-        // next) and scan tiles 2m, 2m + 1 (one chunk) -- two-tile R / S runs like
-        // the default schedule, with the reduce D tiles ahead of the scan.  The
-        // prologue reduces tiles 0 .. D - 1 ((D - 1) / 2 whole chunks + one tile).
-        const int D = -ilv;
-        const int P = (D + 1) / 2;
-        int k0, n;
-        if (q < P) {
-            J.is_scan = false;
-            k0 = 2 * q;
-            n = (q < P - 1) ? 2 : 1;
-        } else {
-            const int qq = q - P, m = qq / 3, r = qq - 3 * m;
-            J.is_scan = r == 2;
-            k0 = r == 2 ? 2 * m : 2 * m + D + r;
-            n = r == 2 ? 2 : 1;
-        }
-        J.c = k0 >> 1;
-        if (J.c >= chunks) {
-            J.c = chunks;
-            J.is_scan = false;
-            J.j0 = J.j1 = 0;
-            J.first = J.last = false;
-            return J;
-        }
-        J.j0 = k0 & 1;
-        J.j1 = J.j0 + n;
-        J.first = J.j0 == 0;
-        J.last = J.j1 == 2;
-        return J;
-    }
-    const int K = chunks * bt;
-    int k;
-    if (q < ilv) {
-        k = q;
-        J.is_scan = false;
-    } else {
-        const int qq = q - ilv;
-        J.is_scan = (qq & 1) != 0;
-        k = J.is_scan ? (qq >> 1) : (qq >> 1) + ilv;
-    }
-    if (k >= K) {
-        J.c = chunks;  // past the end
-        J.is_scan = false;
-        J.j0 = J.j1 = 0;
-        J.first = J.last = false;
-        return J;
-    }
-    J.c = k / bt;
-    const int j = k - J.c * bt;
-    J.j0 = j;
-    J.j1 = j + 1;
-    J.first = j == 0;
-    J.last = j == bt - 1;
-    return J;
 }
 
 // Ring position: slot index and the parity of its current use.
@@ -227,14 +121,11 @@ struct McParams16 {
     int64_t seg_len;        // > 0: segmented scan of contiguous rows of seg_len >= TILE elements
                             // (carries reset at every row start); 0: one 1-D scan
     int lazy_carry;         // Phase II waits for the block carry only at the first tile's emit
-    int jgrp;               // jobs in groups of jgrp chunks (mc_job_g); 1 = chunk by chunk
-    int ilv;                // > 0: tile-interleaved schedule, reduces ilv tiles ahead (mc_job_x)
     int bar_mode;           // chunk barrier: 0 = release-add counter per chunk, then the block sums;
                             // 1 = block sums as epoch-tagged words polled directly (one L2 round
                             // trip after the last publish instead of two)
     int wait_mode;          // mbarrier waits: bit 0 producer / storer, bit 1 compute warps sleep in the
-                            // barrier unit (suspend-time hint) instead of spinning; bit 2: the
-                            // coordinator's and storer's probes use the non-blocking test_wait
+                            // barrier unit (suspend-time hint) instead of spinning
     int shift;              // SHIFT instantiation: the input starts `shift` elements past a 16-byte
                             // boundary; tm_in / the bulk copies address that aligned-down base
     CUtensorMap tm_in1;     // SHIFT, 2-/4-byte inputs: the same view with a one-row box (the row
@@ -824,9 +715,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     const int warp = tid >> 5;
     const McGeom& gm = p.gm;
     const int b = blockIdx.x;
-    const int jgrp = p.jgrp > 1 ? p.jgrp : 1;
-    const int ilv = SEG ? 0 : p.ilv;
-    const int njobs = mc_njobs(gm.chunks, gm.bt, jgrp, ilv);
+    const int njobs = gm.chunks * 2;
     // Per-CTA stall counters (SCAN_DEBUG=4).  Their clock reads cost ~14
     // instructions per 1,024 elements even when off, so they are compiled out of
     // the 1- and 2-byte and shifted instantiations (C2 84.2 -> 86.6 %) unless
@@ -864,11 +753,10 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     }
     __syncthreads();
 
-    // Tiles [t0, t1) of job J (tiles j0..j1-1 of block b of chunk J.c).
-    auto block_tiles = [&](const McJob& J, int& t0, int& t1) {
-        const int base = J.c * gm.chunk_tiles + b * gm.bt;
-        t0 = base + J.j0;
-        t1 = base + J.j1;
+    // Tiles [t0, t1) of block b of chunk c.
+    auto block_tiles = [&](int c, int& t0, int& t1) {
+        t0 = c * gm.chunk_tiles + b * gm.bt;
+        t1 = t0 + gm.bt;
         if (t0 > gm.ntiles) t0 = gm.ntiles;
         if (t1 > gm.ntiles) t1 = gm.ntiles;
     };
@@ -892,11 +780,10 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
             }
             Ring<NB_IN> rin;
             for (int q = 0; q < njobs; ++q) {
-                int t0, t1;
-                const McJob J = mc_job_x(q, gm.chunks, gm.bt, p.ahead, jgrp, ilv);
-                if (J.c >= gm.chunks) continue;
-                const bool is_scan = J.is_scan;
-                block_tiles(J, t0, t1);
+                int c, t0, t1;
+                bool is_scan;
+                mc_job(q, gm.chunks, p.ahead, c, is_scan);
+                block_tiles(c, t0, t1);
                 const uint64_t pol = is_scan ? pol_drop : pol_keep;
                 for (int t = t0; t < t1; ++t, rin.next()) {
                     if (rin.wrapped) {
@@ -955,11 +842,10 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     ptx::mbar_arrive(&out_empty[slot]);
             };
             for (int q = 0; q < njobs; ++q) {
-                int t0, t1;
-                const McJob J = mc_job_x(q, gm.chunks, gm.bt, p.ahead, jgrp, ilv);
-                if (J.c >= gm.chunks) continue;
-                const bool is_scan = J.is_scan;
-                block_tiles(J, t0, t1);
+                int c, t0, t1;
+                bool is_scan;
+                mc_job(q, gm.chunks, p.ahead, c, is_scan);
+                block_tiles(c, t0, t1);
                 if (!is_scan) {
                     if (UNI)
                         for (int t = t0; t < t1; ++t) rin.next();
@@ -968,8 +854,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 for (int t = t0; t < t1; ++t, rin.next(), rout.next()) {
                     const int o = UNI ? rin.s : rout.s;
                     const uint32_t par = UNI ? ((sparity >> o) & 1u) : rout.ph;
-                    if (pend >= 0 && !((p.wait_mode & 4) ? ptx::mbar_test_wait(&store_ready[o], par)
-                                                         : ptx::mbar_try_wait(&store_ready[o], par))) {
+                    if (pend >= 0 && !ptx::mbar_try_wait(&store_ready[o], par)) {
                         // about to block: release the pending slot first
                         ptx::bulk_wait_read<0>();
                         release(pend);
@@ -1037,9 +922,7 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
             // fault-injection build, tests/test_gpu_fuzz.py)
             bool rs_ready = false;
             if (next_pub < gm.chunks && lane == 0)
-                rs_ready = (p.wait_mode & 4)
-                               ? ptx::mbar_test_wait(&rsum_ready[next_pub % RS], (uint32_t)(next_pub / RS) & 1u)
-                               : ptx::mbar_try_wait(&rsum_ready[next_pub % RS], (uint32_t)(next_pub / RS) & 1u);
+                rs_ready = ptx::mbar_try_wait(&rsum_ready[next_pub % RS], (uint32_t)(next_pub / RS) & 1u);
             rs_ready = __shfl_sync(0xffffffffu, rs_ready, 0);
             if (rs_ready) {
                 if (lane == 0) {
@@ -1201,21 +1084,14 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
             seg_s.init(b, gm.bt, p.seg_len);
             seg_dc = ((int64_t)gm.chunk_tiles * TILE) % p.seg_len;
         }
-        const long long tl0 = prof0 ? clock64() : 0;
-        Carry jsum = Carry(0);    // Phase I: this block's sum so far (persists across interleaved jobs)
-        Carry carry = Carry(0);   // Phase II: the running carry of the block being scanned
-        bool have_carry = false;
         for (int q = 0; q < njobs; ++q) {
-            int t0, t1;
-            const McJob J = mc_job_x(q, gm.chunks, gm.bt, p.ahead, jgrp, ilv);
-            if (J.c >= gm.chunks) continue;
-            const int c = J.c;
-            const bool is_scan = J.is_scan;
-            block_tiles(J, t0, t1);
-            const long long tj0 = prof0 ? clock64() : 0;
+            int c, t0, t1;
+            bool is_scan;
+            mc_job(q, gm.chunks, p.ahead, c, is_scan);
+            block_tiles(c, t0, t1);
             if (!is_scan) {
                 // ---------------- Phase I: block reduction r[c][b] ----------------
-                if (J.first) jsum = Carry(0);
+                Carry jsum = Carry(0);
                 if constexpr (SEG) seg_r.job(t0, p.seg_len, seg_dc, gm.n);
                 for (int t = t0; t < t1; ++t, rin.next()) {
                     mbar_wait_prof(&in_full[rin.s], rin.ph, prof0, &s_prof[1], csleep);
@@ -1257,24 +1133,19 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                         s_prof[10] += (unsigned long long)(clock64() - tr0);
                     }
                 }
-                if (J.last) {
-                    jsum = warp_reduce_fixed(jsum);
-                    if (lane == 0) {
-                        s_job_sum[c % RS][cw] = jsum;
-                        ptx::mbar_arrive(&rsum_ready[c % RS]);
-                    }
+                jsum = warp_reduce_fixed(jsum);
+                if (lane == 0) {
+                    s_job_sum[c % RS][cw] = jsum;
+                    ptx::mbar_arrive(&rsum_ready[c % RS]);
                 }
-                if (prof0) s_prof[21] += (unsigned long long)(clock64() - tj0);
             } else {
                 // ---------------- Phase II: scan with the block carry ----------------
                 // The carry is first needed at the first tile's emit: the tile's loads, lane
                 // prefixes and shuffle / warp-total scans run before the wait (lazy carry),
                 // hiding the chunk barrier's latency behind them.  Segmented scans take it
                 // up front (their split-tile path needs it earlier).
-                if (J.first) {
-                    carry = Carry(0);
-                    have_carry = false;
-                }
+                Carry carry = Carry(0);
+                bool have_carry = false;
                 auto get_carry = [&]() {
                     if (!have_carry) {
                         mbar_wait_prof(&carry_ready[c % KC], (uint32_t)(c / KC) & 1u, prof0, &s_prof[0], csleep);
@@ -1409,10 +1280,8 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                     }
                     }  // row start inside the tile / not
                 }
-                if (prof0) s_prof[22] += (unsigned long long)(clock64() - tj0);
             }
         }
-        if (prof0) s_prof[23] += (unsigned long long)(clock64() - tl0);
     }
 
     __syncthreads();

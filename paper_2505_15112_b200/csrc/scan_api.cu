@@ -376,12 +376,6 @@ struct Mc16Variant {
         p.wait_mode = env_int("SCAN_MC_WAIT", sizeof(In) < 4 ? 3 : 1);
         p.bar_mode = env_int("SCAN_MC_BAR", 0);
         p.lazy_carry = env_int("SCAN_MC_LAZY", 0);  // A/B: measured +1.8 points at ahead 1, none at the default
-        p.jgrp = env_int("SCAN_MC_GRP", 1);
-        if (p.jgrp < 1) p.jgrp = 1;
-        while (p.jgrp > 1 && p.jgrp * (p.ahead + 1) > 8) --p.jgrp;  // carry / block-sum rings hold 8 chunks
-        p.ilv = env_int("SCAN_MC_ILV", 0);  // tile-interleaved schedule (A/B), D tiles ahead
-        // two-tile interleave (A/B, SCAN_MC_ILV2 = odd D): needs bt = 2 (checked below)
-        if (env_int("SCAN_MC_ILV2", 0) > 0) p.ilv = -(env_int("SCAN_MC_ILV2", 0) | 1);
         p.seg_len = segmented ? sp.seg_len : 0;
         p.gm.n = n;
         p.gm.g = di.sms < kMaxGrid ? di.sms : kMaxGrid;
@@ -395,7 +389,6 @@ struct Mc16Variant {
         if ((ntiles + (int64_t)p.gm.g * bt64 - 1) / ((int64_t)p.gm.g * bt64) > kMaxChunks)  // counters must fit
             bt64 = (ntiles + (int64_t)kMaxChunks * p.gm.g - 1) / ((int64_t)kMaxChunks * p.gm.g);
         p.gm.bt = (int)bt64;
-        if (p.ilv < 0 && p.gm.bt != 2) p.ilv = 0;  // the two-tile interleave is defined for bt = 2
         p.gm.chunk_tiles = p.gm.g * p.gm.bt;
         p.gm.chunks = (int)((ntiles + p.gm.chunk_tiles - 1) / p.gm.chunk_tiles);
         void* args[] = {&p};
@@ -487,12 +480,6 @@ int launch_mc(const ScanParams& p, cudaStream_t s, const DevInfo& di)
         if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 16, 2, 2, 1>, DT>(p, s, di);
         else return launch_mc_sized<Mc16Variant<DT, 16, 2, 4, 2>, DT>(p, s, di);
     case 7: return launch_mc_sized<Mc16Variant<DT, 16, 2, 3, 0>, DT>(p, s, di);   // unified in-place ring
-    case 30:  // A/B: 8 compute warps, 32-KB fp32 tiles, 5 + 1 slots (more loads in flight)
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 8, 2, 5, 1>, DT>(p, s, di);
-        else return SCAN_ERR_ARG;
-    case 31:  // A/B: 12 compute warps x 1 group, 24-KB fp32 tiles, 6 + 2 slots
-        if constexpr (wide_in) return launch_mc_sized<Mc16Variant<DT, 12, 1, 6, 2>, DT>(p, s, di);
-        else return SCAN_ERR_ARG;
     case 20: {  // A/B: the segmented instantiation on one row
         using V = std::conditional_t<wide_in, Mc16Variant<DT, 12, 2, 3, 1, true>,
                                      std::conditional_t<DT == SCAN_F16_F32, Mc16Variant<DT, 16, 2, 3, 2, true>,

@@ -42,7 +42,7 @@ __device__ __forceinline__ void mbar_wait_prof(uint64_t* bar, uint32_t parity, b
             ptx::mbar_wait(bar, parity);
         return;
     }
-    if (ptx::mbar_test_wait(bar, parity)) return;  // non-blocking: a parked try_wait would hide the wait
+    if (ptx::mbar_try_wait(bar, parity)) return;
     long long t0 = clock64();
     ptx::mbar_wait(bar, parity);
     atomicAdd(acc, (unsigned long long)(clock64() - t0));

@@ -24,7 +24,7 @@ SPEC = {  # config: (input dtype, n, recipe, seed, exclusive, bytes per element 
 }
 NAMES = ["c_wait_carry", "c_wait_in_R", "c_wait_in_S", "c_wait_out_empty", "coord_spin", "storer_wait_ready",
          "storer_bulk_wait", "total", "R_tiles", "S_tiles", "R_cycles", "S_pre", "S_bar", "S_post", "e14", "e15",
-         "e16", "e17", "pub_to_complete", "complete_to_sums", "chunks", "R_jobs", "S_jobs", "job_loop"]
+         "e16", "e17", "pub_to_complete", "complete_to_sums", "chunks"]
 KWS_PARTIALS = 256
 
 

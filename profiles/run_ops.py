@@ -2,7 +2,7 @@
 (profiles/r01_ops_*_full.txt):
     ncu --set full -k regex:<kernel> -s 1 -c 1 python profiles/run_ops.py <op>
 op: split (2^28, fp16 payload + indices), compress (2^28 fp16, no indices), sort (2^24 fp16
-keys), top_p (1024 C4 rows, p=0.9), shard (C5 shard of 2^29 elements: block sums + row-kernel
+keys), sort_rows (512 C4 rows fp32 descending), top_p (1024 C4 rows, p=0.9), shard (C5 shard of 2^29 elements: block sums + row-kernel
 pass), rows_short (2^20 x 32 and 2^15 x 4096 fp32 rows), rows_few (8 x 2^24 fp32 rows:
 segmented MCScan)."""
 import os
@@ -42,6 +42,11 @@ elif op == "sort":
     k = torch.randn(1 << 24, device="cuda").half()
     for _ in range(2):
         S.radix_sort(k)
+elif op == "sort_rows":  # 512 C4 rows, fp32 descending (the top-p sort path's row sort)
+    P = torch.empty((512, 131072), dtype=torch.float32, device="cuda")
+    inputs.fill_device(inputs.F32_SOFTMAX, 3, 0, 512, 131072, P)
+    for _ in range(2):
+        S.radix_sort_rows(P, descending=True)
 elif op == "top_p":
     P = torch.empty((1024, 131072), dtype=torch.float32, device="cuda")
     inputs.fill_device(inputs.F32_SOFTMAX, 3, 0, 1024, 131072, P)
