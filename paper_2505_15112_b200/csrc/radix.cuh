@@ -115,6 +115,9 @@ __device__ __forceinline__ uint32_t digit_of(uint32_t key, int shift, int descen
 // cheaper than MATCH.ANY (measured: 415 -> 333 us for a 2^24 fp16 sort).
 __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid)
 {
+#ifdef RADIX_MATCH  // A/B build: MATCH.ANY (invalid lanes get a unique value: singletons)
+    return __match_any_sync(0xffffffffu, valid ? d : 0x100u | (threadIdx.x & 31u));
+#endif
     uint32_t peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
@@ -259,6 +262,8 @@ __global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
             const uint32_t tdp = s_tdp[tid] + off;
             s_tdp[tid] = tdp;
             s_gb[tid] = tg.row0 + (int64_t)s_dbase[tid] + (int64_t)my_off - (int64_t)tdp;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) s_hist[w][tid] += tdp;  // one staging table
         }
         __syncthreads();
 
@@ -270,7 +275,7 @@ __global__ void __launch_bounds__(kThreads) k_digit_scatter(const DigitParams p)
                 const uint32_t k = ES == 2 ? (key[r] & 0xffffu) : key[r];
                 const uint32_t rk = ES == 2 ? (key[r] >> 16) : rank[ES == 2 ? 0 : r];
                 const uint32_t d = digit_of<KT>(k, p.shift, p.descending);
-                const uint32_t s = s_tdp[d] + s_hist[warp][d] + rk;
+                const uint32_t s = s_hist[warp][d] + rk;
                 st_key[s] = (K)k;
                 if constexpr (IDX_IN) st_idx[s] = ix[r];
                 else st_idx[s] = (int32_t)(e - tg.row0);  // element (or, segmented, column) index
@@ -474,6 +479,11 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
             const uint32_t tdp = s_tdp[tid] + off;
             s_tdp[tid] = tdp;
             s_gb[tid] = tg.row0 + (int64_t)s_dbase[tid] + (int64_t)my_off - (int64_t)tdp;
+            // one staging table: s_hist[w][d] becomes the tile-local start of (warp w,
+            // digit d) -- one bank-conflicted shared load per staged element instead of
+            // two (measured: row sort 19.89 -> 19.24 ms, fp16 sort 0.335 -> 0.329 ms)
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) s_hist[w][tid] += tdp;
         }
         ptx::named_bar_sync(1, kThreads);
 #pragma unroll
@@ -483,7 +493,7 @@ __global__ void __launch_bounds__(kThreads + 32, DigitTmaCfg<ES, IDX_IN>::kCtas)
                 const uint32_t k = ES == 2 ? (key[r] & 0xffffu) : key[r];
                 const uint32_t rk = ES == 2 ? (key[r] >> 16) : s_rank[li];
                 const uint32_t d = digit_of<KT>(k, p.shift, p.descending);
-                const uint32_t st = s_tdp[d] + s_hist[warp][d] + rk;
+                const uint32_t st = s_hist[warp][d] + rk;
                 st_key[st] = (K)k;
                 if constexpr (IDX_IN) st_idx[st] = in_ring ? si[li] : p.idx_in[t0 + li];
                 else st_idx[st] = (int32_t)(t0 + li - tg.row0);
