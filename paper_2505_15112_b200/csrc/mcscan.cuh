@@ -49,7 +49,11 @@
 
 namespace scan {
 
+#ifdef SCAN_MC_PROF
+constexpr int kMcProf = 25;  // [21..24] (prof build): globaltimer at entry, first tile in, last job done, exit
+#else
 constexpr int kMcProf = 21;  // [18..20]: coordinator publish -> complete, complete -> sums loaded, chunks
+#endif
 
 // Block reductions live in the workspace after the header: r[c][b] (8 bytes
 // each, chunk-major); barrier counters in their own region (kWsBarOffset).
@@ -730,6 +734,9 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     const bool prof = kProfRuntime && (p.debug & 4) != 0;
 #endif
     const long long t_start = clock64();
+#ifdef SCAN_MC_PROF
+    const unsigned long long g_entry = ptx::globaltimer();
+#endif
 
     WsHeader* hdr = reinterpret_cast<WsHeader*>(p.ws);
     uint64_t* r_all = reinterpret_cast<uint64_t*>(p.ws + kWsDescOffset);
@@ -738,6 +745,9 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     Out* gout = reinterpret_cast<Out*>(p.out);
 
     if (tid < kMcProf) s_prof[tid] = 0;
+#ifdef SCAN_MC_PROF
+    if (tid == 0) s_prof[21] = g_entry;
+#endif
     if (tid == 0) {
         for (int s = 0; s < NB_IN; ++s) {
             ptx::mbar_init(&in_full[s], 1);
@@ -1095,6 +1105,9 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
                 if constexpr (SEG) seg_r.job(t0, p.seg_len, seg_dc, gm.n);
                 for (int t = t0; t < t1; ++t, rin.next()) {
                     mbar_wait_prof(&in_full[rin.s], rin.ph, prof0, &s_prof[1], csleep);
+#ifdef SCAN_MC_PROF
+                    if (prof0 && s_prof[22] == 0) s_prof[22] = ptx::globaltimer();
+#endif
                     const long long tr0 = prof ? clock64() : 0;
                     const uint8_t* slot = in_ring + rin.s * Cfg::kRingSlot;
                     if (SEG && t == seg_r.tile) {
@@ -1284,8 +1297,14 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
         }
     }
 
+#ifdef SCAN_MC_PROF
+    if (prof && warp == 3 && lane == 0) s_prof[23] = ptx::globaltimer();  // compute warp 0 done
+#endif
     __syncthreads();
     if (prof && tid == 0) s_prof[7] = (unsigned long long)(clock64() - t_start);
+#ifdef SCAN_MC_PROF
+    if (prof && tid == 0) s_prof[24] = ptx::globaltimer();
+#endif
     __syncthreads();
     if (prof && tid < kMcProf && (blockIdx.x + 1) * kMcProf * 8 <= (int)(kWsBarOffset - kWsPartialsOffset))
         reinterpret_cast<unsigned long long*>(p.ws + kWsPartialsOffset)[blockIdx.x * kMcProf + tid] = s_prof[tid];
