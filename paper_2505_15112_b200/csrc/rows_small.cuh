@@ -99,7 +99,11 @@ constexpr int kTileMaxCols = 32;
 constexpr int kTileWords = kThreads * kTileMaxCols;
 __device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
 
-template <int DT>
+// STRIDED: rows at any 16-byte-multiple stride (in and out), cols a multiple of
+// 16 / sizeof(In) and of 4.  The tile's vector q is vector q % V of its row q / V
+// (V vectors per row), so the staged layout -- and the scan phase -- are the same
+// as for contiguous rows; a warp's loads cover whole 16-byte-aligned row pieces.
+template <int DT, bool STRIDED = false>
 __global__ void __launch_bounds__(kThreads) k_rows_tile(const SRParams p)
 {
     using Tr = Traits<DT>;
@@ -121,13 +125,20 @@ __global__ void __launch_bounds__(kThreads) k_rows_tile(const SRParams p)
     // scanned and stored (a thread holds at most kVPT vectors of a tile)
     constexpr int kVPT = kTileMaxCols * kEs / 16;
     uint4 pf[kVPT];
+    const int vin = cols / kPerVec, vout = cols / 4;  // STRIDED: vectors per row in / out
     auto prefetch = [&](int64_t tt) {
         const int64_t g0 = tt * tile_elems;
         const int nv = tt < tiles ? (int)(min(tile_elems, total - g0) / kPerVec) : 0;
 #pragma unroll
         for (int v = 0; v < kVPT; ++v) {
             const int q = tid + v * kThreads;
-            pf[v] = q < nv ? __ldg(reinterpret_cast<const uint4*>(in + g0) + q) : make_uint4(0u, 0u, 0u, 0u);
+            if constexpr (STRIDED) {
+                const int r = q / vin;
+                const In* src = in + (tt * kThreads + r) * p.in_stride + (q - r * vin) * kPerVec;
+                pf[v] = q < nv ? __ldg(reinterpret_cast<const uint4*>(src)) : make_uint4(0u, 0u, 0u, 0u);
+            } else {
+                pf[v] = q < nv ? __ldg(reinterpret_cast<const uint4*>(in + g0) + q) : make_uint4(0u, 0u, 0u, 0u);
+            }
         }
     };
     prefetch(blockIdx.x);
@@ -145,7 +156,8 @@ __global__ void __launch_bounds__(kThreads) k_rows_tile(const SRParams p)
                 for (int j = 0; j < kPerVec; ++j) s_v[pad32(q * kPerVec + j)] = widen(e[j]);
             }
         }
-        for (int i = nvec * kPerVec + tid; i < ne; i += kThreads) s_v[pad32(i)] = widen(in[f0 + i]);
+        if constexpr (!STRIDED)  // (STRIDED: whole vectors only)
+            for (int i = nvec * kPerVec + tid; i < ne; i += kThreads) s_v[pad32(i)] = widen(in[f0 + i]);
         __syncthreads();
         prefetch(t + gridDim.x);
         // 2. thread tid scans row tid of the tile, in place
@@ -171,9 +183,15 @@ __global__ void __launch_bounds__(kThreads) k_rows_tile(const SRParams p)
             Out* e = reinterpret_cast<Out*>(&w);
 #pragma unroll
             for (int j = 0; j < 4; ++j) e[j] = narrow(s_v[pad32(q * 4 + j)], (Out*)nullptr);
-            reinterpret_cast<uint4*>(out + f0)[q] = w;
+            if constexpr (STRIDED) {
+                const int r = q / vout;
+                *reinterpret_cast<uint4*>(out + (t * kThreads + r) * p.out_stride + (q - r * vout) * 4) = w;
+            } else {
+                reinterpret_cast<uint4*>(out + f0)[q] = w;
+            }
         }
-        for (int i = nvo * 4 + tid; i < ne; i += kThreads) out[f0 + i] = narrow(s_v[pad32(i)], (Out*)nullptr);
+        if constexpr (!STRIDED)
+            for (int i = nvo * 4 + tid; i < ne; i += kThreads) out[f0 + i] = narrow(s_v[pad32(i)], (Out*)nullptr);
         __syncthreads();
     }
 }

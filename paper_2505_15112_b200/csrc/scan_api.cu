@@ -642,11 +642,24 @@ int launch_rows_small(const ScanParams& sp, cudaStream_t s, const DevInfo& di)
     p.exclusive = sp.exclusive;
     const bool contig = sp.in_stride == sp.seg_len && sp.out_stride == sp.seg_len &&
                         ((reinterpret_cast<uintptr_t>(sp.in) | reinterpret_cast<uintptr_t>(sp.out)) & 15) == 0;
-    if (sp.seg_len <= kTileMaxCols && contig && env_int("SCAN_ROWS_TILE", 1)) {
+    // strided rows of whole 16-byte vectors (every row start 16-byte aligned, in and out)
+    // and at least 64 bytes of input per row: measured (profiles/r02c_rows_tiny.txt) fp32 x 32
+    // 45 -> 50 %, int32 x 32 44 -> 55 %, fp16 x 32 36 -> 61 % of the copy peak against the
+    // shuffle kernel, fp32 x 16 even, fp32 x 8 (32-byte rows) 45 -> 36 % (kept on the shuffles)
+    constexpr int kEsIn = (int)sizeof(typename Traits<DT>::In);
+    const bool strided_vec = !contig && sp.seg_len * kEsIn >= 64 && sp.seg_len % (16 / kEsIn) == 0 &&
+                             sp.seg_len % 4 == 0 &&
+                             (sp.in_stride * kEsIn) % 16 == 0 && (sp.out_stride * 4) % 16 == 0 &&
+                             ((reinterpret_cast<uintptr_t>(sp.in) | reinterpret_cast<uintptr_t>(sp.out)) & 15) == 0 &&
+                             env_int("SCAN_ROWS_TILE_STRIDED", 1);
+    if (sp.seg_len <= kTileMaxCols && (contig || strided_vec) && env_int("SCAN_ROWS_TILE", 1)) {
         int64_t grid = (sp.num_segs + kThreads - 1) / kThreads;
         const int64_t cap = (int64_t)di.sms * 6;  // 34 KB of shared memory per CTA
         if (grid > cap) grid = cap;
-        k_rows_tile<DT><<<(unsigned)grid, kThreads, 0, s>>>(p);
+        if (contig)
+            k_rows_tile<DT><<<(unsigned)grid, kThreads, 0, s>>>(p);
+        else
+            k_rows_tile<DT, true><<<(unsigned)grid, kThreads, 0, s>>>(p);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return cudaGetLastError() == cudaSuccess ? SCAN_OK : SCAN_ERR_CUDA;
     }

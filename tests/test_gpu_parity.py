@@ -406,6 +406,30 @@ def test_rows_tiny_contiguous(cuda, oracle, inputs_mod, dt, exclusive):
 
 @pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
 @pytest.mark.parametrize("exclusive", [False, True])
+def test_rows_tiny_strided(cuda, oracle, inputs_mod, dt, exclusive):
+    """Strided rows of <= 32 columns, every row start 16-byte aligned in and out
+    (the staged tile kernel's strided addressing) and not (the shuffle kernel):
+    ragged row counts, input and output strides both wider than the row."""
+    es = {"i32": 4, "f32": 4, "f16": 2, "i8": 1}[dt]
+    for R, C, S_in, S_out in [(1000, 4, 8, 12), (777, 8, 24, 16), (513, 16, 48, 20), (300, 32, 64, 36),
+                              (257, 32, 32 + 16 // es, 40), (999, 12, 16, 16), (65, 5, 8, 8)]:
+        x = host_input(inputs_mod, dt, R * S_in, seed=R * 5 + C).reshape(R, S_in)
+        xd = to_dev(x, dt)[:, :C]
+        outb = torch.empty((R, S_out), dtype=torch.int32 if dt in ("i32", "i8") else torch.float32, device="cuda")
+        out = outb[:, :C]
+        cuda.rows(xd, exclusive=exclusive, out=out)
+        torch.cuda.synchronize()
+        xc = np.ascontiguousarray(x[:, :C])
+        if dt in ("i32", "i8"):
+            assert np.array_equal(out.cpu().numpy(), oracle.rows(xc, dt, exclusive=exclusive)), (R, C)
+        else:
+            y64, a64, _ = oracle.rows(xc, dt, exclusive=exclusive)
+            bad, worst, at = oracle.check_f32(out.cpu().numpy(), y64, a64)
+            assert bad == 0, (R, C, worst, at)
+
+
+@pytest.mark.parametrize("dt", ["i32", "f32", "f16", "i8"])
+@pytest.mark.parametrize("exclusive", [False, True])
 def test_rows_short_and_few_long(cuda, oracle, inputs_mod, dt, exclusive):
     """Row shapes of every row path: tiny rows (segmented warp scan, several
     rows per warp), short rows (a warp per row), few long rows (one MCScan per
