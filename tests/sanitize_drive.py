@@ -61,9 +61,10 @@ def main():
                 got = (S.exclusive if exc else S.inclusive)(xd)
                 check(f"{tag} {dt} {'exc' if exc else 'inc'} n={n}", got,
                       (oracle.exclusive if exc else oracle.inclusive)(x, dt), dt)
-        for R, C, tag in ((2048, 32, "k_rows_tile"), (64, 20, "k_rows_tiny (strided)"), (300, 700, "k_rows_warp"),
+        for R, C, tag in ((2048, 32, "k_rows_tile"), (64, 20, "k_rows_tiny (strided)"),
+                          (600, 32, "k_rows_tile (strided, aligned)"), (300, 700, "k_rows_warp"),
                           (148, 16384, "k_rowscan16"), (3, 1 << 19, "k_mcscan16 SEG")):
-            S_ = C + 4 if "strided" in tag else C
+            S_ = C + (16 if "aligned" in tag else 4) if "strided" in tag else C
             X = inputs.fill_host(KIND[dt], R + C, 0, R * S_).reshape(R, S_)
             Xd = dev(X, dt)[:, :C]
             got = S.rows(Xd)
@@ -119,6 +120,29 @@ def main():
         print(f"{'top-p ' + method:48s} {'ok' if ok else 'MISMATCH'}")
         if not ok:
             FAIL.append("top-p " + method)
+    # top-p retries: a superset overflow (tiny early maximum), a nucleus past the first
+    # window (redo), and C4 rows with a 5-octave first window (most rows redone)
+    C = 131072
+    rng = np.random.default_rng(11)
+    ra = np.zeros(C, np.float32)
+    ra[:2048] = 1e-12
+    ra[2048:22048] = np.float32(0.01 * 2.0 ** -15)
+    ra[rng.choice(np.arange(30000, C), 3000, replace=False)] = (0.005 + 0.005 * rng.random(3000)).astype(np.float32)
+    rb = np.zeros(C, np.float32)
+    rb[77] = 0.01
+    rb[rng.choice(np.arange(1000, C), 5000, replace=False)] = np.float32(0.01 * 2.0 ** -12.6)
+    for name, Pr, w0 in (("top-p select retries", np.stack([ra, rb]), None), ("top-p select forced redo", P, "40")):
+        if w0:
+            os.environ["SCAN_TOPP_W0"] = w0
+        ur = np.random.default_rng(5).random(len(Pr)).astype(np.float32)
+        tk, _ = S.top_p_sample(dev(Pr, "f32"), 0.9, dev(ur, "f32"))
+        os.environ.pop("SCAN_TOPP_W0", None)
+        tk = tk.cpu().numpy()
+        ok = all(int(tk[r]) == oracle.top_p_sample(Pr[r], float(np.float32(0.9)), float(ur[r]))[0]
+                 for r in range(len(Pr)))
+        print(f"{name:48s} {'ok' if ok else 'MISMATCH'}")
+        if not ok:
+            FAIL.append(name)
     os.environ["SCAN_ROWS_TC"] = "1"
     X = inputs.fill_host(inputs.I8_FULL, 9, 0, 4 * 16384).reshape(4, 16384)
     check("k_rowscan_tc int8 (tcgen05 kind::i8)", S.rows(dev(X, "i8")), np.stack([oracle.inclusive(r, "i8") for r in X]),
