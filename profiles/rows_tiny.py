@@ -1,5 +1,10 @@
-import os, sys
-sys.path.insert(0, os.getcwd())
+"""Strided tiny-row scans (rows of <= 32 columns at a wider row stride): CUDA-event time per
+scan_rows call, median of 10, for a few shapes (profiles/r02c_rows_tiny.txt).
+    [SCAN_LIB=...] [SCAN_ROWS_TILE_STRIDED=0] python profiles/rows_tiny.py
+"""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2505_15112_b200 as S
 lib = os.environ.get("SCAN_LIB", "libscan.so")
