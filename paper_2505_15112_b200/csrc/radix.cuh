@@ -121,8 +121,9 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid)
     uint32_t peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
-        const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        peers &= ((d >> b) & 1u) ? bb : ~bb;
+        const bool bit = (d & (1u << b)) != 0u;  // one LOP3 to a predicate (was a shift + compare)
+        const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bb : ~bb;
     }
     return peers;
 }
