@@ -376,9 +376,12 @@ class Run:
             self.step()
         torch.cuda.synchronize()
         graph = None
-        if graph_opt or (graph_opt is None and self.cfg == "C1"):
-            # latency-bound sizes: the K steps captured back to back in one CUDA
-            # graph, so the timed region measures the GPU, not Python + ctypes
+        if graph_opt or (graph_opt is None and not self.sharded):
+            # the K steps captured back to back in one CUDA graph, so the timed
+            # region measures the GPU, not Python + ctypes and per-launch stream
+            # gaps (same-box A/B, profiles/r02d_graph_ab.txt: C2 89.6 -> 91.7 %,
+            # C3 99.4 -> 100.5 %, C5 +0.3 %); the sharded path keeps eager steps
+            # for its per-phase CUDA events
             graph = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream()
             side.wait_stream(stream)
@@ -739,7 +742,7 @@ def main():
     ap.add_argument("--no-other-configs", action="store_true",
                     help="skip timing the other BASELINE.json configs after the main line")
     ap.add_argument("--graph", dest="graph", action="store_true", default=None,
-                    help="replay each step from a CUDA graph (default: on for C1 only)")
+                    help="replay the timed steps from a CUDA graph (default: on unless sharded)")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
