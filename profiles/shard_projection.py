@@ -10,7 +10,10 @@ The NCCL all-gather of G x 8 bytes is not included (NVLink latency, ~10-20 us);
 rss_peer_exchange has no all-gather at all (the totals travel inside the two
 kernels), its slot writes here are local (emulated peers) -- over NVLink each
 rank's publish adds G remote 16-byte stores.
-CUDA events, median of 5 after 2 warm-ups; rank 1's shard (nonzero carry).
+CUDA events, median of 5 single calls after 2 warm-ups (per_gpu_us: includes the
+host launch latency of every call) and the per-call time of 10 calls replayed from one
+CUDA graph (graph_per_gpu_us: the device's back-to-back rate); rank 1's shard
+(nonzero carry).
 
     python profiles/shard_projection.py [C5|C3 ...]
 """
@@ -43,6 +46,32 @@ def timed(fn, reps=5, warm=2):
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e-3)
     return statistics.median(ts)
+
+
+def timed_graph(fn, reps=10):
+    """Per-call time of `reps` calls captured back to back in one CUDA graph
+    (the device's back-to-back rate, without per-call host launch latency)."""
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        for _ in range(reps):
+            fn()
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(3):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.replay()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3 / reps)
+    del g
+    return min(ts)
 
 
 def main():
@@ -91,8 +120,11 @@ def main():
             for name, fn in (("rss_blocks", new), ("rss_peer_exchange", peer), ("rss_mcscan", old),
                              ("single_pass", single)):
                 t = timed(fn)
+                tg = timed_graph(fn)
                 rec[name] = {"per_gpu_us": round(t * 1e6, 1), "per_gpu_pct_alg": round(100 * m * bpe / t / 1e9 / peak, 1),
-                             "aggregate_GBps": round(G * m * bpe / t / 1e9, 0)}
+                             "aggregate_GBps": round(G * m * bpe / t / 1e9, 0),
+                             "graph_per_gpu_us": round(tg * 1e6, 1),
+                             "graph_per_gpu_pct_alg": round(100 * m * bpe / tg / 1e9 / peak, 1)}
             print(json.dumps(rec), flush=True)
             out.append(rec)
             del x, y, ws
