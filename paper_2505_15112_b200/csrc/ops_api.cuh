@@ -297,7 +297,8 @@ int sort_digits(const void* keys, void* keys_out, int32_t* idx_out, int64_t n, i
     p.descending = descending != 0;
     p.cols = cols;
     p.tpr = (int)tpr;
-    const int64_t g_count = (int64_t)di.sms * 4 < nt ? (int64_t)di.sms * 4 : nt;
+    p.count_pf = env_int("SCAN_RADIX_PF", 1);  // measured: row sort 18.65 -> 18.55 ms, fp32 2^26 2.428 -> 2.415 ms
+    const int64_t g_count = (int64_t)di.sms * RADIX_COUNT_CTAS < nt ? (int64_t)di.sms * RADIX_COUNT_CTAS : nt;
     const int64_t g_scat = (int64_t)di.sms * occ < nt ? (int64_t)di.sms * occ : nt;
     const void* src_k = keys;
     const int32_t* src_i = nullptr;

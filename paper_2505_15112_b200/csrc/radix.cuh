@@ -65,6 +65,7 @@ struct DigitParams {
     // the digit bases included; indices are column indices.
     int64_t cols;
     int tpr;
+    int count_pf;            // k_digit_count: L2 bulk prefetch of the CTA's next tile (tiles ahead, 0 = off)
 };
 
 // Geometry of tile t: first element, element count, the row's first element,
@@ -129,35 +130,81 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid)
 }
 
 // ---- counts per (digit, tile) --------------------------------------------------
+#ifndef RADIX_COUNT_CTAS
+#define RADIX_COUNT_CTAS 3
+#endif
 template <int KT, int ES>
-__global__ void __launch_bounds__(kThreads) k_digit_count(const DigitParams p)
+__global__ void __launch_bounds__(kThreads, RADIX_COUNT_CTAS) k_digit_count(const DigitParams p)
 {
-    __shared__ uint32_t s_hist[kWarps][kDigits];
+    // two warp-private histogram sets, used by alternate tiles: the thread that
+    // sums a digit's 16 warp counts clears them for the tile after next, so each
+    // tile needs ONE CTA barrier (between its atomics and its sums)
+    __shared__ uint32_t s_hist[2][kWarps][kDigits];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x) {
-        for (int i = tid; i < kWarps * kDigits; i += kThreads) (&s_hist[0][0])[i] = 0;
-        __syncthreads();
-        const TileGeom tg = tile_geom(p, t);
-        const int l0 = warp * (kRounds * 32);
-        uint32_t key[kRounds];
-#pragma unroll
-        for (int r = 0; r < kRounds; ++r) {
-            const int li = l0 + r * 32 + lane;
-            key[r] = li < tg.mt ? load_key<KT, ES>(p.keys_in, tg.t0 + li) : 0u;
+    // one thread prefetches the CTA's tile count_pf steps ahead into L2, so the
+    // next iteration's key loads meet L2 latency instead of HBM latency
+    auto prefetch = [&](int tp) {
+        if (tp < p.ntiles) {
+            const TileGeom pg = tile_geom(p, tp);
+            const uintptr_t a = (uintptr_t)p.keys_in + (uintptr_t)(pg.t0 * ES);
+            const uintptr_t a0 = (a + 15) & ~(uintptr_t)15, a1 = (a + (uintptr_t)pg.mt * ES) & ~(uintptr_t)15;
+            if (a1 > a0) ptx::l2_prefetch_bulk(reinterpret_cast<const void*>(a0), (uint32_t)(a1 - a0));
         }
+    };
+    if (tid == 0)
+        for (int k = 1; k < p.count_pf; ++k) prefetch(blockIdx.x + k * gridDim.x);
+    for (int i = tid; i < 2 * kWarps * kDigits; i += kThreads) (&s_hist[0][0][0])[i] = 0;
+    __syncthreads();
+    int hb = 0;
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, hb ^= 1) {
+        if (tid == 0 && p.count_pf > 0) prefetch(t + p.count_pf * gridDim.x);
+        const TileGeom tg = tile_geom(p, t);
+        uint32_t(&h)[kDigits] = s_hist[hb][warp];
+        const char* kb = reinterpret_cast<const char*>(p.keys_in) + tg.t0 * ES;
+        if (tg.mt == kTile && ((uintptr_t)kb & 15) == 0) {
+            // whole, 16-byte aligned tile: 16-byte loads (counting ignores order)
+            constexpr int KPV = 16 / ES;                 // keys per 16-byte vector
+            constexpr int NV = kRounds / KPV;            // vectors per thread
+            uint4 v[NV];
 #pragma unroll
-        for (int r = 0; r < kRounds; ++r) {
-            const int li = l0 + r * 32 + lane;
-            if (li < tg.mt) atomicAdd(&s_hist[warp][digit_of<KT>(key[r], p.shift, p.descending)], 1u);
+            for (int r = 0; r < NV; ++r) v[r] = __ldg(reinterpret_cast<const uint4*>(kb) + r * kThreads + tid);
+#pragma unroll
+            for (int r = 0; r < NV; ++r) {
+                const uint32_t w[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if constexpr (ES == 4) {
+                        atomicAdd(&h[digit_of<KT>(w[j], p.shift, p.descending)], 1u);
+                    } else {
+                        atomicAdd(&h[digit_of<KT>(w[j] & 0xffffu, p.shift, p.descending)], 1u);
+                        atomicAdd(&h[digit_of<KT>(w[j] >> 16, p.shift, p.descending)], 1u);
+                    }
+                }
+            }
+        } else {
+            const int l0 = warp * (kRounds * 32);
+            uint32_t key[kRounds];
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r) {
+                const int li = l0 + r * 32 + lane;
+                key[r] = li < tg.mt ? load_key<KT, ES>(p.keys_in, tg.t0 + li) : 0u;
+            }
+#pragma unroll
+            for (int r = 0; r < kRounds; ++r) {
+                const int li = l0 + r * 32 + lane;
+                if (li < tg.mt) atomicAdd(&h[digit_of<KT>(key[r], p.shift, p.descending)], 1u);
+            }
         }
         __syncthreads();
         for (int d = tid; d < kDigits; d += kThreads) {
             uint32_t c = 0;
 #pragma unroll
-            for (int w = 0; w < kWarps; ++w) c += s_hist[w][d];
+            for (int w = 0; w < kWarps; ++w) {
+                c += s_hist[hb][w][d];
+                s_hist[hb][w][d] = 0;
+            }
             p.counts[tg.c0 + (int64_t)d * tg.dstride] = c;
         }
-        __syncthreads();
     }
 }
 
