@@ -195,6 +195,22 @@ __device__ __forceinline__ void cluster_sync_all()
 {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Split cluster barrier: arrive early (every CTA has started), wait later.
+__device__ __forceinline__ void cluster_arrive_relaxed()
+{
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait()
+{
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+}
+// Write a 64-bit word into the shared memory of CTA `rank` of this cluster.
+__device__ __forceinline__ void st_dsmem_u64(void* local_smem_ptr, uint32_t rank, uint64_t v)
+{
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(ptx::smem_u32(local_smem_ptr)), "r"(rank));
+    asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(remote), "l"(v) : "memory");
+}
 // Read a 64-bit word from the shared memory of CTA `rank` of this cluster.
 __device__ __forceinline__ uint64_t ld_dsmem_u64(const void* local_smem_ptr, uint32_t rank)
 {
@@ -389,6 +405,7 @@ struct ScanParams {
     int tma_out;            // same for output
     int static_sched;       // one tile per segment: no tickets, no look-back
     int cluster;            // > 0: small-n mode, one tile per CTA of ONE cluster, carries via DSMEM
+    int cl_push;            // cluster mode: aggregates pushed to the higher CTAs (one cluster barrier)
     int debug;              // bit 0: skip look-back (timing only; wrong results); bit 1: spin without
                             // nanosleep; bit 2: per-CTA stall counters into the workspace
     int shift;              // MCScan SHIFT: `in` is this many elements past a 16-byte boundary
@@ -441,6 +458,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
     __shared__ Carry s_prefix;
     __shared__ uint32_t s_epoch;
     __shared__ uint64_t s_cl_agg;  // cluster mode: this CTA's tile aggregate (Carry bits)
+    __shared__ uint64_t s_cl_in[16];  // cluster push mode: slot r = the aggregate of CTA r < this CTA
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
@@ -486,6 +504,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
     // in the stream may start launching now; it waits in ITS griddepcontrol.wait
     // until this grid has completed and flushed.  No-ops without the attribute.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // cluster push mode: announce this CTA has started (its shared memory may
+    // receive the lower CTAs' aggregates once every CTA has announced)
+    if (p.cluster && p.cl_push) cluster_arrive_relaxed();
     if (tid == 0) {
         for (int s = 0; s < STAGES; ++s) ptx::mbar_init(&full_bar[s], 1);
         ptx::fence_mbar_init();
@@ -619,15 +640,37 @@ __global__ void __launch_bounds__(THREADS, MINB) k_scan_tiles(const ScanParams p
             // its aggregate in its own shared memory; after a cluster barrier
             // warp 0 sums the aggregates of the lower-ranked CTAs over DSMEM
             // (fixed lane-tree order) -- no global descriptors, no atomics.
-            cluster_sync_all();
-            if (warp == 0) {
-                const uint32_t rank = cluster_ctarank();
-                Carry v = Carry(0);
-                if ((uint32_t)lane < rank) v = carry_from_bits<Carry>(ld_dsmem_u64(&s_cl_agg, (uint32_t)lane));
-                v = warp_reduce_fixed(v);
-                if (lane == 0) s_prefix = s_prefix + v;
+            if (p.cl_push) {
+                // push: every CTA of the cluster has started (the early arrive's
+                // phase), so lane q > rank of warp 0 stores this CTA's aggregate
+                // into CTA q's slot; after ONE barrier the lower aggregates are
+                // local, and no CTA touches another's shared memory afterwards
+                cluster_wait();
+                if (warp == 0) {
+                    __syncwarp();
+                    const uint32_t rank = cluster_ctarank();
+                    if ((uint32_t)lane > rank && lane < p.cluster)
+                        st_dsmem_u64(&s_cl_in[rank], (uint32_t)lane, s_cl_agg);
+                }
+                cluster_sync_all();
+                if (warp == 0) {
+                    const uint32_t rank = cluster_ctarank();
+                    Carry v = Carry(0);
+                    if ((uint32_t)lane < rank) v = carry_from_bits<Carry>(s_cl_in[lane]);
+                    v = warp_reduce_fixed(v);
+                    if (lane == 0) s_prefix = s_prefix + v;
+                }
+            } else {
+                cluster_sync_all();
+                if (warp == 0) {
+                    const uint32_t rank = cluster_ctarank();
+                    Carry v = Carry(0);
+                    if ((uint32_t)lane < rank) v = carry_from_bits<Carry>(ld_dsmem_u64(&s_cl_agg, (uint32_t)lane));
+                    v = warp_reduce_fixed(v);
+                    if (lane == 0) s_prefix = s_prefix + v;
+                }
+                cluster_sync_all();  // no CTA leaves while another may still read its shared memory
             }
-            cluster_sync_all();  // no CTA leaves while another may still read its shared memory
         }
         // The output staging buffer we are about to fill must no longer be
         // read by the bulk store issued OSTAGES tiles ago.
