@@ -363,6 +363,45 @@ class Run:
         else:
             (S.exclusive if "exclusive" in w["ops"] else S.inclusive)(self.x, out=self.out)
 
+    def sustained(self, seconds=0.7):
+        """The same step back to back for `seconds` after 0.5 s of idle, every step
+        between its own CUDA events: the rate of the first steps (burst: SM clocks at
+        their maximum) against the rate once the 1 kW power cap has pulled the clocks
+        down (profiles/r02e_copy_sustained.txt: a plain copy keeps its rate, the fp32
+        MCScan loses ~10 %).  Context for `value`, whose K steps follow an idle GPU."""
+        import torch
+        stream = torch.cuda.current_stream()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        self.step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        n = max(20, int(1e3 * seconds / max(a.elapsed_time(b), 1e-3)))
+        clocks = ClockSampler(self.dev.index)
+        clocks.start()
+        time.sleep(0.5)
+        evs = []
+        for i in range(n + 1):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            evs.append(e)
+            if i < n:
+                self.step()
+        torch.cuda.synchronize()
+        clk = clocks.stop()
+        ts = [evs[i].elapsed_time(evs[i + 1]) for i in range(n)]
+        k = max(1, n // 20)
+        first, last = statistics.median(ts[1:1 + k]), statistics.median(ts[-k:])
+        nbytes = self.total_elems * self.w["bpe"] * self.scans_per_step
+        peak, _ = peaks()
+        return {"steps": n, "seconds": round(sum(ts) * 1e-3, 3),
+                "first_ms_per_step": round(first, 5), "first_frac": round(nbytes / first / 1e6 / peak, 4),
+                "last_ms_per_step": round(last, 5), "value": round(nbytes / last / 1e6, 1), "unit": "GB/s",
+                "frac": round(nbytes / last / 1e6 / peak, 4), "clocks": clk,
+                "note": f"first = median of steps 1..{k} after 0.5 s idle, value / last / frac = median of the "
+                        f"final {k} steps; per-step CUDA events, eager launches"}
+
     def c1_cold_us(self, steps):
         """C1 with a cold L2: 2 * steps scans (inclusive, exclusive alternating),
         each on its own copy of the input and its own output, captured in one
@@ -521,6 +560,11 @@ def run_ours(args, rank, world, local_rank):
     roof, value, ms_per_step = m["roof"], m["value"], m["ms_per_step"]
     peak = roof["peak"]
 
+    # ---- burst vs sustained: the same step for ~0.7 s (power cap), single GPU
+    sustained = None
+    if world == 1 and cfg != "C1" and not args.no_sustained:
+        sustained = run.sustained()
+
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -598,6 +642,8 @@ def run_ours(args, rank, world, local_rank):
                                    "(pass 1), NCCL all-gather of the G totals, carry, scan_shard_scan (pass 2)")
         line.update({"ceilings": ceilings, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": m["launches"],
                      "clocks": m["clocks"]})
+        if sustained is not None:
+            line["sustained"] = sustained
         if others is not None:
             line["other_configs"] = others
         print(json.dumps(line), flush=True)
@@ -771,6 +817,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunk", type=int, default=1 << 26, help="elements per host-streaming chunk")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sustained", action="store_true", help="skip the ~0.7 s burst-vs-sustained leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
                     help="gloo: test the multi-rank harness with ranks sharing one GPU (numbers not comparable)")
