@@ -56,3 +56,19 @@ def test_default_line_keys_on_c1():
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0 and {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["n_gpus"] == 1 and d["higher_is_better"] is True
+
+
+@pytest.mark.gpu
+def test_sustained_leg_and_c1_cold_on_c2():
+    """The burst-vs-sustained leg (DESIGN 8.1) on C2, and C1's cold-L2 figure from
+    `other_configs` is covered by the default run; here: the `sustained` object."""
+    r = _run(["--config", "C2", "--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--no-other-configs",
+              "--no-ceilings", "--no-e2e"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    s = d["sustained"]
+    assert {"steps", "seconds", "first_ms_per_step", "first_frac", "last_ms_per_step", "value", "unit", "frac",
+            "clocks"} <= set(s)
+    assert s["steps"] >= 20 and s["seconds"] > 0.3 and s["unit"] == "GB/s"
+    assert 0.2 < s["frac"] <= s["first_frac"] * 1.05  # the sustained rate never beats the burst by more than noise
+    assert s["value"] == pytest.approx(2 ** 28 * 6 / s["last_ms_per_step"] / 1e6, rel=1e-3)
