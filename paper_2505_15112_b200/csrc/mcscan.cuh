@@ -691,9 +691,17 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     // shared-memory provenance (LDS / STS on 32-bit addresses); through an integer
     // round trip it loses it and emits generic LD.E / ST.E with 64-bit address
     // math for every slot access.  Measured (DESIGN 5.1, same box, 3 runs each):
-    // shared C2 83.0 -> 86.6 %, C3 90.5 -> 91.5 %, shifted C5 -> 91.1 %, but the
-    // aligned 4-byte kernel (C5) 92.1 -> 90.4 % -- it keeps the generic form.
+    // shared C2 83.0 -> 86.6 %, C3 90.5 -> 91.5 %, shifted C5 -> 91.1 %.  The
+    // aligned 4-byte kernel (C5) kept the generic form until the fourth session of
+    // round 2 because it is 1.5 points faster in a burst (92.1 vs 90.6 %); under
+    // the power cap the lighter form holds 91.6 % where the generic one falls to
+    // 82-88 % (DESIGN 8.1), so every instantiation now takes the shared form
+    // (-DSCAN_MC_GENERIC4 restores the old one for A/B).
+#ifdef SCAN_MC_GENERIC4
     constexpr bool kGenericBase = (SZ == 4 && SH == 0 && !SEG);
+#else
+    constexpr bool kGenericBase = false;
+#endif
     uint8_t* const smem =
         kGenericBase ? reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023)
                      : smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -721,13 +729,15 @@ __global__ void __launch_bounds__((3 + NC) * 32, 1) k_mcscan16(const __grid_cons
     const int b = blockIdx.x;
     const int njobs = gm.chunks * 2;
     // Per-CTA stall counters (SCAN_DEBUG=4).  Their clock reads cost ~14
-    // instructions per 1,024 elements even when off, so they are compiled out of
-    // the 1- and 2-byte and shifted instantiations (C2 84.2 -> 86.6 %) unless
-    // -DSCAN_MC_PROF; the aligned 4-byte kernel keeps them: without them C5
-    // measured 92.0 -> 90.7 % (same box, 3 runs each) -- like the shared-address
-    // form below, anything that speeds up its compute warps costs C5 DRAM
-    // efficiency (DESIGN 5.1).
+    // instructions per 1,024 elements even when off (C2 84.2 -> 86.6 % without
+    // them), so they are compiled in only with -DSCAN_MC_PROF (profiles/
+    // mc_counters.py, mc_timeline.py) or, for the aligned 4-byte kernel, with
+    // -DSCAN_MC_GENERIC4 (the pre-8.1 form of that kernel, which kept them).
+#ifdef SCAN_MC_GENERIC4
     constexpr bool kProfRuntime = (sizeof(In) == 4 && SH == 0 && !SEG);
+#else
+    constexpr bool kProfRuntime = false;
+#endif
 #ifdef SCAN_MC_PROF
     const bool prof = (p.debug & 4) != 0;
 #else
