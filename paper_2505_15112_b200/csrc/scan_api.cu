@@ -370,7 +370,10 @@ struct Mc16Variant {
         p.exclusive = sp.exclusive;
         p.debug = debug_bits();
         p.ahead = ahead < 1 ? 1 : (ahead > 4 ? 4 : ahead);
-        p.l2 = env_int("SCAN_MC_L2", 0);
+        // L2 policy of the Phase-I read: evict_last for 1- and 2-byte inputs; 4-byte
+        // inputs take evict_normal (bit 0) since the lighter compute path (DESIGN 8.1:
+        // C5 burst 90.6 -> 91.9 %, sustained 91.7 -> 91.5 %; C2 / C3 lose 0.4-0.6 with it)
+        p.l2 = env_int("SCAN_MC_L2", sizeof(In) == 4 ? 1 : 0);
         // mbarrier waits (measured, DESIGN 5.1): the producer / storer sleep in
         // the barrier unit instead of spinning, and for 1- and 2-byte inputs (more
         // instructions per byte) the compute warps too; SCAN_MC_WAIT overrides
